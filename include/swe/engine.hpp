@@ -1,0 +1,392 @@
+// swe/engine.hpp -- the drop-in time loop (reference: /root/reference/proj/
+// include/swe/engine.hpp:24-394), executed on a B200 through the C-ABI of
+// swe_dev.h.  Same types, signatures, exception types and message texts as
+// the reference, so callers (the reference's cases.hpp, bench.hpp, CLI and
+// tests) compile and behave unchanged; there is no CPU path -- every step runs
+// the CUDA kernels, and a missing/failed device raises swe::device_error.
+//
+// Device residency: the mesh is uploaded (and renumbered on the device) once
+// per Mesh object and cached; advance_step() keeps the reference's
+// host-resident Simulation contract (state up, one step, state down), while
+// run() keeps the state on the device for the whole loop and only downloads at
+// snapshots and at the end (the paper's transfer-minimisation rule).
+#pragma once
+
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <functional>
+#include <limits>
+#include <map>
+#include <memory>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "swe/core.hpp"
+#include "swe/mesh.hpp"
+#include "swe_dev.h"
+
+namespace swe {
+
+/// Reference plugin point (engine.hpp:24-31).  The B200 engine always runs
+/// on the device; `device` selects the CUDA ordinal.  kind/threads are
+/// accepted for source compatibility and do not change results (the
+/// reference's backends are bitwise identical too).
+struct BackendSpec {
+  enum class Kind { sequential, parallel };
+  Kind kind = Kind::sequential;
+  int threads = 1;
+  bool deterministic = true;
+  int device = 0;
+
+  bool is_parallel() const { return kind == Kind::parallel && threads > 1; }
+};
+
+struct FieldState {
+  std::vector<double> h, qx, qy;
+  void resize(int n) {
+    h.assign(n, 0.0);
+    qx.assign(n, 0.0);
+    qy.assign(n, 0.0);
+  }
+  int size() const { return static_cast<int>(h.size()); }
+  ConservedState cell(int i) const { return {h[i], qx[i], qy[i]}; }
+  void set_cell(int i, const ConservedState& u) {
+    h[i] = u.h;
+    qx[i] = u.qx;
+    qy[i] = u.qy;
+  }
+};
+
+struct EdgeFluxes {
+  std::vector<Flux3> left, right;
+  void resize(int n) {
+    left.assign(n, {});
+    right.assign(n, {});
+  }
+};
+
+struct MassLedger {
+  double initial_volume = 0.0;
+  double clipped_volume = 0.0;
+  long clip_events = 0;
+};
+
+struct Simulation {
+  FieldState current, next;
+  double t = 0.0;
+  long step = 0;
+  MassLedger ledger;
+};
+
+struct StepStats {
+  long step = 0;
+  double t = 0.0;
+  double dt = 0.0;
+  double max_speed = 0.0;
+  double mass = 0.0;
+  double wall_flux_ms = 0.0;
+  double wall_update_ms = 0.0;
+};
+
+struct RunStats {
+  long steps = 0;
+  double t_final = 0.0;
+  double mass_initial = 0.0;
+  double mass_final = 0.0;
+  double mass_drift_rel = 0.0;
+  double min_dt = 0.0;
+  double mean_dt = 0.0;
+  long clip_events = 0;
+  double clipped_volume = 0.0;
+  double wall_flux_s = 0.0;
+  double wall_update_s = 0.0;
+  double wall_total_s = 0.0;
+  std::vector<StepStats> series;
+};
+
+struct RunOptions {
+  double t_end = 0.0;
+  double snapshot_interval = 0.0;
+  long max_steps = 100'000'000;
+  bool record_series = true;
+  bool per_step_timing = false;
+  std::function<void(const FieldState&, double t, long step)> on_snapshot;
+};
+
+namespace detail {
+
+/// Device context of one Mesh (uploaded + renumbered once).
+class DeviceMesh {
+ public:
+  DeviceMesh(const Mesh& m, const PhysParams& p, int device) : device_(device), params_(p) {
+    const int C = m.n_cells(), E = m.n_edges();
+    std::vector<double> cx(C), cy(C), nx(E), ny(E);
+    std::vector<int> ce(3 * static_cast<size_t>(C)), cs(3 * static_cast<size_t>(C));
+    for (int c = 0; c < C; ++c) {
+      cx[c] = m.cell_centroid[c].x;
+      cy[c] = m.cell_centroid[c].y;
+      for (int k = 0; k < 3; ++k) {
+        ce[3 * static_cast<size_t>(c) + k] = m.cell_edges[c][k].edge;
+        cs[3 * static_cast<size_t>(c) + k] = m.cell_edges[c][k].sign;
+      }
+    }
+    for (int e = 0; e < E; ++e) {
+      nx[e] = m.edge_normal[e].x;
+      ny[e] = m.edge_normal[e].y;
+    }
+    swe_mesh_view v{};
+    v.n_cells = C;
+    v.n_edges = E;
+    v.area = m.cell_area.data();
+    v.inradius = m.cell_inradius.data();
+    v.bed = m.cell_bed.data();
+    v.manning = m.cell_manning.data();
+    v.cx = cx.data();
+    v.cy = cy.data();
+    v.cell_edge = ce.data();
+    v.cell_sign = cs.data();
+    v.edge_left = m.edge_left.data();
+    v.edge_right = m.edge_right.data();
+    v.nx = nx.data();
+    v.ny = ny.data();
+    v.len = m.edge_length.data();
+    const swe_params sp = to_c(p);
+    check(swe_dev_create(&v, &sp, device, 0, &ctx_), "swe_dev_create");
+    fingerprint_ = print(m);
+  }
+  ~DeviceMesh() { swe_dev_destroy(ctx_); }
+  DeviceMesh(const DeviceMesh&) = delete;
+  DeviceMesh& operator=(const DeviceMesh&) = delete;
+
+  swe_dev_ctx* ctx() const { return ctx_; }
+  bool matches(const Mesh& m, const PhysParams& p, int device) const {
+    return device == device_ && print(m) == fingerprint_ && same(p, params_);
+  }
+
+  static swe_params to_c(const PhysParams& p) { return {p.g, p.h_dry, p.cfl, p.dt_max, p.h_ref}; }
+
+  static void check(int rc, const char* what) {
+    if (rc == SWE_OK) return;
+    throw device_error(std::string(what) + ": " + swe_dev_strerror(rc) + " (" +
+                       swe_dev_last_error() + ")");
+  }
+
+ private:
+  static bool same(const PhysParams& a, const PhysParams& b) {
+    return a.g == b.g && a.h_dry == b.h_dry && a.cfl == b.cfl && a.dt_max == b.dt_max &&
+           a.h_ref == b.h_ref;
+  }
+  static std::vector<const void*> print(const Mesh& m) {
+    return {m.cell_area.data(), m.cell_bed.data(), m.cell_manning.data(), m.edge_length.data(),
+            m.cell_edges.data(), reinterpret_cast<const void*>(static_cast<intptr_t>(m.n_cells())),
+            reinterpret_cast<const void*>(static_cast<intptr_t>(m.n_edges()))};
+  }
+  swe_dev_ctx* ctx_ = nullptr;
+  int device_;
+  PhysParams params_;
+  std::vector<const void*> fingerprint_;
+};
+
+inline std::map<const Mesh*, std::unique_ptr<DeviceMesh>>& device_cache() {
+  static std::map<const Mesh*, std::unique_ptr<DeviceMesh>> cache;
+  return cache;
+}
+
+/// Process-wide cache: one device context per (Mesh, params, device).
+inline DeviceMesh& device_mesh(const Mesh& m, const PhysParams& p, int device) {
+  auto& slot = device_cache()[&m];
+  if (!slot || !slot->matches(m, p, device)) {
+    slot.reset();
+    slot = std::make_unique<DeviceMesh>(m, p, device);
+  }
+  return *slot;
+}
+
+inline void upload(DeviceMesh& dm, const FieldState& s, double t, long step) {
+  DeviceMesh::check(swe_dev_set_state(dm.ctx(), s.h.data(), s.qx.data(), s.qy.data(), t, step),
+                    "swe_dev_set_state");
+}
+
+inline void download(DeviceMesh& dm, FieldState& s) {
+  double t;
+  long long step;
+  DeviceMesh::check(swe_dev_get_state(dm.ctx(), s.h.data(), s.qx.data(), s.qy.data(), &t, &step),
+                    "swe_dev_get_state");
+}
+
+// reference message templates (std::to_string formatting, engine.hpp:169,
+// :206, :294-296)
+[[noreturn]] inline void raise(const swe_status& st, const FieldState* next) {
+  (void)next;
+  switch (st.code) {
+    case SWE_NONFINITE_SPEED:
+      throw numeric_error("stable_dt: non-finite velocity in cell " + std::to_string(st.index));
+    case SWE_NEGATIVE_DEPTH:
+      throw numeric_error("compute_fluxes: negative depth at edge " + std::to_string(st.index));
+    case SWE_BLOWUP:
+      throw numeric_error("advance_step: numeric blowup at step " + std::to_string(st.step) +
+                          ", cell " + std::to_string(st.index) + ", dt " + std::to_string(st.dt) +
+                          " (h=" + std::to_string(st.h) + ")");
+    default:
+      throw device_error(std::string("device step failed: ") + swe_dev_strerror(st.code) + " (" +
+                         swe_dev_last_error() + ")");
+  }
+}
+
+}  // namespace detail
+
+/// Drops the device copy of a mesh (call before destroying or mutating it).
+inline void release_device_mesh(const Mesh& m) { detail::device_cache().erase(&m); }
+
+/// Volume integral of the depth (engine.hpp:128-132), reduced on the device
+/// in a fixed order (matches the reference's serial sum to round-off).
+inline double total_mass(const FieldState& s, const Mesh& mesh,
+                         const PhysParams& p = PhysParams{}, int device = 0) {
+  auto& dm = detail::device_mesh(mesh, p, device);
+  detail::upload(dm, s, 0.0, 0);
+  double m = 0.0;
+  detail::DeviceMesh::check(swe_dev_total_mass(dm.ctx(), &m), "swe_dev_total_mass");
+  return m;
+}
+
+/// One flux evaluation per edge (engine.hpp:138-170), on the device.
+inline void compute_fluxes(const FieldState& s, const Mesh& mesh, const PhysParams& p,
+                           const BackendSpec& backend, EdgeFluxes& out) {
+  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  detail::upload(dm, s, 0.0, 0);
+  if (static_cast<int>(out.left.size()) != mesh.n_edges()) out.resize(mesh.n_edges());
+  swe_status st{};
+  const int rc = swe_dev_compute_fluxes(dm.ctx(), reinterpret_cast<double*>(out.left.data()),
+                                        reinterpret_cast<double*>(out.right.data()), &st);
+  if (rc != SWE_OK) detail::raise(st, nullptr);
+}
+
+/// One explicit Euler step truncated to land on t_end (engine.hpp:226-319).
+/// Host-resident contract: sim.current is uploaded, stepped on the device and
+/// the result swapped back in.  `fluxes` is not filled (the edge records stay
+/// on the device); use compute_fluxes() to inspect them.
+inline StepStats advance_step(Simulation& sim, const Mesh& mesh, const PhysParams& p,
+                              const BackendSpec& backend, double t_end, EdgeFluxes& fluxes,
+                              StepStats* timing = nullptr) {
+  (void)fluxes;
+  using clock = std::chrono::steady_clock;
+  const auto t0 = clock::now();
+  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  detail::upload(dm, sim.current, sim.t, sim.step);
+  detail::DeviceMesh::check(
+      swe_dev_set_ledger(dm.ctx(), sim.ledger.clipped_volume, sim.ledger.clip_events),
+      "swe_dev_set_ledger");
+  swe_step_record rec{};
+  swe_status st{};
+  const int rc = swe_dev_step(dm.ctx(), t_end, &rec, &st);
+  if (rc != SWE_OK) detail::raise(st, nullptr);
+  if (static_cast<int>(sim.next.h.size()) != mesh.n_cells()) sim.next.resize(mesh.n_cells());
+  detail::download(dm, sim.next);
+  long long events = 0;
+  detail::DeviceMesh::check(swe_dev_get_ledger(dm.ctx(), &sim.ledger.clipped_volume, &events),
+                            "swe_dev_get_ledger");
+  sim.ledger.clip_events = static_cast<long>(events);
+  std::swap(sim.current, sim.next);
+  sim.t = rec.t;
+  sim.step = static_cast<long>(rec.step);
+  StepStats out;
+  out.step = sim.step;
+  out.t = sim.t;
+  out.dt = rec.dt;
+  out.max_speed = rec.max_speed;
+  if (timing)
+    timing->wall_update_ms =
+        std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+  return out;
+}
+
+/// The time loop (engine.hpp:335-394) with the state resident on the device.
+inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
+                    const BackendSpec& backend, const RunOptions& opt) {
+  using clock = std::chrono::steady_clock;
+  if (!(opt.t_end > 0.0)) throw config_error("run: t_end must be > 0");
+  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  swe_dev_ctx* ctx = dm.ctx();
+
+  RunStats rs;
+  detail::upload(dm, sim.current, sim.t, sim.step);
+  detail::DeviceMesh::check(swe_dev_total_mass(ctx, &rs.mass_initial), "swe_dev_total_mass");
+  sim.ledger.initial_volume = rs.mass_initial;
+  detail::DeviceMesh::check(
+      swe_dev_set_ledger(ctx, sim.ledger.clipped_volume, sim.ledger.clip_events),
+      "swe_dev_set_ledger");
+
+  if (opt.on_snapshot) opt.on_snapshot(sim.current, sim.t, sim.step);
+  double next_snapshot = opt.snapshot_interval > 0.0 ? sim.t + opt.snapshot_interval
+                                                     : std::numeric_limits<double>::infinity();
+  rs.min_dt = std::numeric_limits<double>::infinity();
+  double dt_sum = 0.0;
+  const auto run_start = clock::now();
+  std::vector<swe_step_record> recs(1 << 16);
+  if (static_cast<int>(sim.next.h.size()) != mesh.n_cells()) sim.next.resize(mesh.n_cells());
+
+  while (sim.t < opt.t_end) {
+    if (sim.step >= opt.max_steps)
+      throw numeric_error("run: exceeded max_steps=" + std::to_string(opt.max_steps) +
+                          " before reaching t_end (t=" + std::to_string(sim.t) + ")");
+    const double snap = opt.on_snapshot ? next_snapshot : std::numeric_limits<double>::infinity();
+    long long n = 0;
+    swe_status st{};
+    const auto b0 = clock::now();
+    const int rc = swe_dev_advance(ctx, opt.t_end, opt.max_steps, snap, recs.data(),
+                                   static_cast<long long>(recs.size()), &n, &st);
+    rs.wall_update_s += std::chrono::duration<double>(clock::now() - b0).count();
+    for (long long i = 0; i < n; ++i) {
+      const swe_step_record& r = recs[static_cast<size_t>(i)];
+      rs.min_dt = std::min(rs.min_dt, r.dt);
+      dt_sum += r.dt;
+      if (opt.record_series) {
+        StepStats s;
+        s.step = static_cast<long>(r.step);
+        s.t = r.t;
+        s.dt = r.dt;
+        s.max_speed = r.max_speed;
+        s.mass = r.mass;
+        rs.series.push_back(s);
+      }
+    }
+    double t;
+    long long step;
+    detail::DeviceMesh::check(swe_dev_get_state(ctx, nullptr, nullptr, nullptr, &t, &step),
+                              "swe_dev_get_state");
+    sim.t = t;
+    sim.step = static_cast<long>(step);
+    if (rc != SWE_OK) {
+      detail::download(dm, sim.current);
+      detail::raise(st, nullptr);
+    }
+    if (opt.on_snapshot && n > 0 && (sim.t >= opt.t_end || sim.t >= next_snapshot - 1e-12)) {
+      detail::download(dm, sim.current);
+      opt.on_snapshot(sim.current, sim.t, sim.step);
+      if (opt.snapshot_interval > 0.0)
+        while (next_snapshot <= sim.t) next_snapshot += opt.snapshot_interval;
+    }
+  }
+  detail::download(dm, sim.current);
+  long long events = 0;
+  detail::DeviceMesh::check(swe_dev_get_ledger(ctx, &sim.ledger.clipped_volume, &events),
+                            "swe_dev_get_ledger");
+  sim.ledger.clip_events = static_cast<long>(events);
+
+  rs.steps = sim.step;
+  rs.t_final = sim.t;
+  rs.mass_final = rs.series.empty() ? 0.0 : rs.series.back().mass;
+  if (rs.series.empty()) detail::DeviceMesh::check(swe_dev_total_mass(ctx, &rs.mass_final), "mass");
+  rs.mass_drift_rel = rs.mass_initial != 0.0 ? (rs.mass_final - rs.mass_initial) / rs.mass_initial
+                                             : rs.mass_final;
+  rs.mean_dt = rs.steps > 0 ? dt_sum / rs.steps : 0.0;
+  if (!std::isfinite(rs.min_dt)) rs.min_dt = 0.0;
+  rs.clip_events = sim.ledger.clip_events;
+  rs.clipped_volume = sim.ledger.clipped_volume;
+  rs.wall_total_s = std::chrono::duration<double>(clock::now() - run_start).count();
+  return rs;
+}
+
+}  // namespace swe

@@ -1,0 +1,166 @@
+/*
+ * swe_dev.h -- C-ABI of the B200 explicit HLLC shallow-water step.
+ *
+ * This is the drop-in boundary for the reference's hot path
+ * (/root/reference/proj/include/swe/engine.hpp).  Plain pointers and sizes,
+ * no C++ or torch types; every entry point returns an int status (SWE_OK = 0)
+ * and never throws.  Host C++ (include/swe/engine.hpp) maps the codes back to
+ * the reference's exception types and message texts; Python reaches the same
+ * symbols through ctypes (paper_1807_00672_b200/_lib.py).
+ *
+ * Numbering: every array crossing this boundary is in the REFERENCE numbering
+ * (the cell/edge order build_mesh produces, mesh.hpp:121-240).  The device
+ * renumbers cells and edges internally for locality (Morton order of
+ * centroids) and permutes state on upload/download; error indices are mapped
+ * back to reference numbering (lowest index wins, as the sequential backend).
+ *
+ * Threading: one context is driven from one host thread (the reference's
+ * Simulation is not re-entrant either, SPEC.md "Concurrency Model").
+ */
+#ifndef SWE_DEV_H
+#define SWE_DEV_H
+
+#ifndef SWE_API
+#if defined(__GNUC__)
+#define SWE_API __attribute__((visibility("default")))
+#else
+#define SWE_API
+#endif
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct swe_dev_ctx swe_dev_ctx;
+
+/* swe::PhysParams (core.hpp:36-42) */
+typedef struct {
+  double g, h_dry, cfl, dt_max, h_ref;
+} swe_params;
+
+/* The arrays of swe::Mesh the step consumes (mesh.hpp:33-61), as SoA views
+ * in reference numbering.  cx/cy (cell centroids) drive the locality
+ * renumbering; pass NULL to keep the reference order. */
+typedef struct {
+  int n_cells, n_edges;
+  const double* area;     /* [C] cell_area */
+  const double* inradius; /* [C] cell_inradius */
+  const double* bed;      /* [C] cell_bed */
+  const double* manning;  /* [C] cell_manning */
+  const double* cx;       /* [C] cell_centroid.x (optional) */
+  const double* cy;       /* [C] cell_centroid.y (optional) */
+  const int* cell_edge;   /* [3C] cell_edges[c][k].edge, CCW local order */
+  const int* cell_sign;   /* [3C] cell_edges[c][k].sign (+1 left, -1 right) */
+  const int* edge_left;   /* [E] */
+  const int* edge_right;  /* [E] -1 (kBoundary) for reflective walls */
+  const double* nx;       /* [E] edge_normal.x */
+  const double* ny;       /* [E] edge_normal.y */
+  const double* len;      /* [E] edge_length */
+} swe_mesh_view;
+
+enum {
+  SWE_OK = 0,
+  SWE_NONFINITE_SPEED = 1, /* stable_dt: non-finite velocity in cell N (engine.hpp:205-206) */
+  SWE_NEGATIVE_DEPTH = 2,  /* compute_fluxes: negative depth at edge N (engine.hpp:168-169) */
+  SWE_BLOWUP = 3,          /* advance_step: numeric blowup (engine.hpp:292-297) */
+  SWE_CUDA = 4,            /* CUDA runtime failure (message via swe_dev_last_error) */
+  SWE_NCCL = 5,            /* multi-device exchange failure */
+  SWE_INVALID = 6          /* bad argument / inconsistent mesh view */
+};
+
+/* Outcome of a step call.  index is a reference-numbered cell or edge; on
+ * SWE_BLOWUP, step/dt/h carry the values the reference prints. */
+typedef struct {
+  int code;
+  long long index;
+  long long step;
+  double dt;
+  double h;
+} swe_status;
+
+/* One row of RunStats::series (engine.hpp:99-107, without wall clocks). */
+typedef struct {
+  long long step;
+  double t, dt, max_speed, mass;
+} swe_step_record;
+
+/* create flags */
+#define SWE_FLAG_IDENTITY_ORDER 1u /* skip the Morton renumbering */
+#define SWE_FLAG_NO_GRAPH 2u       /* advance with plain launches, no CUDA graph */
+
+/* Uploads the mesh, renumbers it on the device, allocates the double-buffered
+ * state and edge records.  device = CUDA ordinal. */
+SWE_API int swe_dev_create(const swe_mesh_view* mesh, const swe_params* params, int device,
+                   unsigned flags, swe_dev_ctx** out);
+SWE_API int swe_dev_destroy(swe_dev_ctx* ctx);
+
+/* Host state in/out (reference numbering); copies are synchronous.  set_state
+ * also resets the CFL cache so the next step recomputes it from this state. */
+SWE_API int swe_dev_set_state(swe_dev_ctx* ctx, const double* h, const double* qx, const double* qy,
+                      double t, long long step);
+SWE_API int swe_dev_get_state(swe_dev_ctx* ctx, double* h, double* qx, double* qy, double* t,
+                      long long* step);
+/* Same, with DEVICE pointers (reference numbering) -- no host copies. */
+SWE_API int swe_dev_set_state_device(swe_dev_ctx* ctx, const double* d_h, const double* d_qx,
+                             const double* d_qy, double t, long long step);
+SWE_API int swe_dev_get_state_device(swe_dev_ctx* ctx, double* d_h, double* d_qx, double* d_qy);
+
+/* The clip ledger (engine.hpp:85-89). */
+SWE_API int swe_dev_get_ledger(swe_dev_ctx* ctx, double* clipped_volume, long long* clip_events);
+SWE_API int swe_dev_set_ledger(swe_dev_ctx* ctx, double clipped_volume, long long clip_events);
+
+/* One advance_step (engine.hpp:226-319): CFL from the current state, truncated
+ * to land on t_end, flux, update, friction, clamp.  rec may be NULL. */
+SWE_API int swe_dev_step(swe_dev_ctx* ctx, double t_end, swe_step_record* rec, swe_status* st);
+
+/* The run() time loop body (engine.hpp:355-380) on the device: steps while
+ * t < t_end, step < max_steps and t < next_snapshot - 1e-12, at most
+ * max_records steps; one record per step into series (host array, may be
+ * NULL when max_records is given only as a bound).  The whole loop is one
+ * CUDA graph launch (conditional WHILE node).  *n_done = steps taken. */
+SWE_API int swe_dev_advance(swe_dev_ctx* ctx, double t_end, long long max_steps, double next_snapshot,
+                    swe_step_record* series, long long max_records, long long* n_done,
+                    swe_status* st);
+
+/* Exactly n steps (t_end = +inf semantics of the bench harness,
+ * bench.hpp:91-110), asynchronous on the context stream: no host sync, no
+ * record download.  Status is checked by the next synchronous call. */
+SWE_API int swe_dev_advance_n_async(swe_dev_ctx* ctx, long long n, double t_end);
+SWE_API int swe_dev_synchronize(swe_dev_ctx* ctx, swe_status* st);
+
+/* compute_fluxes (engine.hpp:138-170) on the current state; left/right are
+ * [3E] Flux3 arrays in reference numbering. */
+SWE_API int swe_dev_compute_fluxes(swe_dev_ctx* ctx, double* left, double* right, swe_status* st);
+
+/* total_mass (engine.hpp:128-132) of the current state (fixed-order tree sum). */
+SWE_API int swe_dev_total_mass(swe_dev_ctx* ctx, double* mass);
+
+/* Kernel-level timing: when enabled, swe_dev_advance_n_async launches without
+ * a graph and brackets every kernel with CUDA events; times accumulate per
+ * kernel (ms): [0] face, [1] cell, [2] finalize, [3] cfl. */
+SWE_API int swe_dev_set_profiling(swe_dev_ctx* ctx, int on);
+SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launches, int n);
+
+/* cudaStream_t of the context (as void*), for events on the launching stream. */
+SWE_API void* swe_dev_stream(swe_dev_ctx* ctx);
+/* Device bytes held by the context. */
+SWE_API long long swe_dev_memory_bytes(swe_dev_ctx* ctx);
+/* Kernels launched by this process through any context. */
+SWE_API long long swe_dev_launch_count(void);
+
+/* Point physics on the device over arrays (kernel-level parity):
+ * kind 0 hllc(l,r,n), 1 wall(l,n), 2 edge combine(l,r,z,n) -> out[6],
+ * 3 friction(l, z[0]=n_manning, z[1]=dt), 4 pow(h, 4/3) (l[0]=h).
+ * l, r: [3n]; z: [2n]; nrm: [2n]; out: [3n] (kind 2: [6n], kind 4: [n]). */
+SWE_API int swe_dev_point_eval(int kind, long long n, const swe_params* params, const double* l,
+                       const double* r, const double* z, const double* nrm, double* out);
+
+SWE_API const char* swe_dev_strerror(int code);
+/* Last CUDA/argument error message of this thread. */
+SWE_API const char* swe_dev_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

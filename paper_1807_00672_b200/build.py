@@ -1,0 +1,88 @@
+"""In-tree build of the native library and the test-only oracle.
+
+    python -m paper_1807_00672_b200.build        # or __graft_entry__.build()
+
+Products (git-ignored, travel to the GPU box with the snapshot):
+  paper_1807_00672_b200/libswe_b200.so   CUDA kernels (sm_100a) + C-ABI
+                                         (include/swe_dev.h, include/swe_host.h)
+  tests/cpp/api_driver                   C++ drop-in API driver (include/swe/*.hpp)
+  oracle/liboracle.so, oracle/_ref/libswe_ref.so   test-only checkers
+"""
+from __future__ import annotations
+
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+ROOT = PKG.parent
+CSRC = PKG / "csrc"
+INC = ROOT / "include"
+BUILD = PKG / "_build"
+LIB = PKG / "libswe_b200.so"
+
+NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# --fmad=false: the reference is built with -ffp-contract=off
+# (CMakeLists.txt:17-18); no contraction keeps every FP64 op bit-identical.
+NVFLAGS = ["-O3", "-lineinfo", "--fmad=false", "-std=c++17", "-Xcompiler", "-fPIC",
+           "-Xcompiler", "-fvisibility=hidden", f"-I{INC}", f"-I{CSRC}"]
+CXXFLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-fvisibility=hidden",
+            f"-I{INC}", "-I/usr/local/cuda/include"]
+
+
+def _stale(target: Path, deps) -> bool:
+    if not target.exists():
+        return True
+    t = target.stat().st_mtime
+    return any(Path(d).stat().st_mtime > t for d in deps)
+
+
+def _run(cmd, verbose):
+    if verbose:
+        print(" ".join(str(c) for c in cmd), flush=True)
+    subprocess.run([str(c) for c in cmd], check=True)
+
+
+def build_library(verbose: bool = False, force: bool = False) -> Path:
+    BUILD.mkdir(exist_ok=True)
+    headers = list(CSRC.glob("*.cuh")) + list(INC.glob("*.h")) + list((INC / "swe").glob("*.hpp"))
+    cu = CSRC / "swe_dev.cu"
+    cu_o = BUILD / "swe_dev.o"
+    host = CSRC / "host_abi.cpp"
+    host_o = BUILD / "host_abi.o"
+    if force or _stale(cu_o, [cu, *headers]):
+        _run([NVCC, *ARCH, *NVFLAGS, "-c", cu, "-o", cu_o], verbose)
+    if force or _stale(host_o, [host, *headers]):
+        _run(["g++", *CXXFLAGS, "-c", host, "-o", host_o], verbose)
+    if force or _stale(LIB, [cu_o, host_o]):
+        _run([NVCC, *ARCH, "-shared", "-o", LIB, cu_o, host_o], verbose)
+    return LIB
+
+
+def build_api_driver(verbose: bool = False, force: bool = False) -> Path:
+    src = ROOT / "tests" / "cpp" / "api_driver.cpp"
+    out = ROOT / "tests" / "cpp" / "api_driver"
+    if not src.exists():
+        return out
+    headers = list((INC / "swe").glob("*.hpp")) + list(INC.glob("*.h"))
+    if force or _stale(out, [src, LIB, *headers]):
+        _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", f"-I{INC}", src, "-o", out,
+              f"-L{PKG}", "-lswe_b200", f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_1807_00672_b200"],
+             verbose)
+    return out
+
+
+def build_oracle(verbose: bool = False) -> None:
+    _run(["make", "-s", "-C", ROOT / "oracle"], verbose)
+
+
+def build_all(verbose: bool = False, force: bool = False) -> None:
+    build_library(verbose, force)
+    build_api_driver(verbose, force)
+    build_oracle(verbose)
+
+
+if __name__ == "__main__":
+    build_all(verbose=True, force="--force" in sys.argv)
