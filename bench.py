@@ -1,0 +1,365 @@
+#!/usr/bin/env python3
+"""Benchmark: explicit HLLC shallow-water steps on B200 (BASELINE.json metric
+"cell-updates/sec (HLLC SWE, 10M tris) ... % of HBM roofline").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config channel] [--scale 1.0]
+
+Workload (default): BASELINE.json configs[2] -- the 10M-triangle synthetic
+meandering river channel with bathymetry and Manning n = 0.03 on an
+unstructured (jittered, randomly renumbered) mesh, 7162 x 716 generator grid =
+10,255,984 cells.  A "step" is one explicit Euler step of the whole mesh
+(CFL reduction + face fluxes + cell update + friction + clamp), as the
+reference's bench harness counts it (bench.hpp:173: cells * steps / wall).
+
+value     K steps with the state resident in HBM (one CUDA graph launch),
+          device time (CUDA events on the solver's stream), max over ranks.
+e2e       the same K steps through the public C-ABI from pinned HOST buffers:
+          upload of the initial state, the K-step run with its per-step stats
+          records copied back, download of the final state -- all inside the
+          timed region (the reference run()'s contract, engine.hpp:335-394).
+roofline  the dominant kernel's algorithmic bytes per launch (SURVEY.md §8(d):
+          face 64 B/edge + 32 B/cell, cell 64 B/edge + 84 B/cell) / its mean
+          CUDA-event duration over a profiled pass of the same K steps.
+cpu_baseline  the reference itself (oracle/_ref, OpenMP, all host threads) on
+          a bounded sample of the same workload, its own phase timers.
+--impl reference   the reference CPU implementation alone on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "cell-updates/sec (HLLC SWE, 10M tris)"
+UNIT = "cell-updates/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+CONFIG_NOTE = {
+    "channel": "BASELINE configs[2]: 10M-triangle meandering channel, bathymetry + Manning n=0.03",
+    "sloping_wet_dry": "BASELINE configs[3]: 10M-triangle dam break onto a dry sloping bed, n=0.03",
+    "three_mounds_friction": "BASELINE configs[1]: 1M-triangle three-mound dam break, n=0.03",
+    "circular_dam_break": "BASELINE configs[0]: ~10k-triangle circular dam break, flat frictionless",
+    "weak_square": "BASELINE configs[4]: weak-scaling square water drop",
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", default="channel", choices=list(CONFIG_NOTE))
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0,
+                    help="target CPU work of the cpu_baseline sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+        self.window = None
+
+    def start(self):
+        """Start sampling (before the warm-up) and wait for the first sample."""
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            t0 = time.time()
+            while not self.rows and time.time() - t0 < 10:
+                time.sleep(0.05)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), [x.strip() for x in line.split(",")]))
+
+    def mark(self, t0, t1):
+        self.window = (t0, t1)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        rows = self.rows
+        where = "during the timed region"
+        if self.window:
+            inside = [r for r in rows if self.window[0] <= r[0] <= self.window[1] + 0.05]
+            if inside:
+                rows = inside
+            else:  # region shorter than the sampling period: nearest samples
+                mid = 0.5 * (self.window[0] + self.window[1])
+                rows = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
+                where = "nearest samples to a timed region shorter than the 50 ms sampling period"
+        rows = [r for _, r in rows]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        num = lambda v: v.replace(".", "", 1).isdigit()  # noqa: E731
+        sm = [float(r[0]) for r in rows if num(r[0])]
+        mx = [float(r[1]) for r in rows if len(r) > 1 and num(r[1])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows), "window": where}
+
+
+def load_peaks():
+    if PEAKS.exists():
+        p = json.loads(PEAKS.read_text())
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def build_workload(name, scale):
+    from paper_1807_00672_b200 import api
+    t0 = time.perf_counter()
+    sc = api.make_scenario(name, scale=scale, unstructured=True)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    return sc, mesh, time.perf_counter() - t0
+
+
+def workload_config(name, sc, mesh, world, note_extra=None):
+    cfg = {"workload": f"{name} ({CONFIG_NOTE[name]})", "cells": mesh.n_cells,
+           "edges": mesh.n_edges, "boundary_edges": mesh.n_boundary_edges,
+           "mesh": "unstructured: jittered nodes, random diagonals, random node/cell numbering",
+           "l2": "inputs larger than L2 (state + mesh ~= 300 B/cell >> 126 MB)",
+           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"}
+    if note_extra:
+        cfg.update(note_extra)
+    return cfg
+
+
+def reference_threads():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+
+
+def time_reference(sc, mesh, steps, warmup, threads):
+    """The reference (oracle/_ref, unmodified headers) on the same mesh and
+    initial state; phase timers of engine.hpp:314-317 as bench.hpp:105-110."""
+    from oracle.pyoracle import RefOracle
+    ref = RefOracle()
+    t0 = time.perf_counter()
+    rm = ref.build_mesh(sc.raw.nodes, sc.raw.triangles, sc.bed, sc.manning)
+    setup_s = time.perf_counter() - t0
+    st = sc.state
+    if warmup > 0:
+        rm.advance(st.h, st.qx, st.qy, t_end=1.7976931348623157e308, nsteps=warmup, threads=threads)
+    r = rm.advance(st.h, st.qx, st.qy, t_end=1.7976931348623157e308, nsteps=steps, threads=threads)
+    if r["rc"] != 0:
+        raise RuntimeError(f"reference failed: {r['error']}")
+    phase_s = r["flux_s"] + r["update_s"]
+    return mesh.n_cells * steps / phase_s, phase_s, setup_s
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from oracle.pyoracle import RefOracle
+    if not RefOracle.available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libswe_ref.so was not built (needs /root/reference)"}))
+        return
+    sc, mesh, _ = build_workload(args.config, args.scale)
+    threads = reference_threads()
+    value, phase_s, setup_s = time_reference(sc, mesh, args.steps, args.warmup, threads)
+    sample = (f"{args.steps} timed steps (after {args.warmup} warm-up) of the full "
+              f"{mesh.n_cells}-cell workload, reference build with -O3 -fopenmp "
+              f"-ffp-contract=off, {threads} OpenMP threads, phase timers")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * phase_s / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(args.config, sc, mesh, 1),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1807_00672_b200 import api
+
+    rank, local, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    sc, mesh, setup_s = build_workload(args.config, args.scale)
+    C, E = mesh.n_cells, mesh.n_edges
+    t0 = time.perf_counter()
+    solver = api.DeviceSolver(mesh, device=local)
+    create_s = time.perf_counter() - t0
+    solver.set_state(sc.state)
+    horizon = 1.7976931348623157e308  # bench.hpp:91 (fixed-step throughput mode)
+    W, K = max(3, args.warmup), args.steps
+    clk = ClockSampler(local).start()
+    solver.advance(t_end=horizon, max_steps=W)
+    _, step0 = solver.clock()
+
+    stream = torch.cuda.ExternalStream(solver.stream, device=local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = api.launch_count()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    w0 = time.time()
+    ev0.record(stream)
+    recs = solver.advance(t_end=horizon, max_steps=step0 + K)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    clk.mark(w0, time.time())
+    clk.stop()
+    launches = api.launch_count() - launches0
+    assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
+    ms = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        dist.barrier()
+    value = world * C * K / (ms / 1e3)
+
+    # kernel-level timing: same K steps, plain launches with events per kernel
+    solver.set_profiling(True)
+    solver.advance_n_async(K, t_end=horizon)
+    solver.synchronize()
+    kt = solver.kernel_times()
+    solver.set_profiling(False)
+    face_ms = kt["face"][0] / max(1, kt["face"][1])
+    cell_ms = kt["cell"][0] / max(1, kt["cell"][1])
+    fin_ms = kt["finalize"][0] / max(1, kt["finalize"][1])
+    peak, peak_src = load_peaks()
+    face_bytes = 64 * E + 32 * C
+    cell_bytes = 64 * E + 84 * C
+    dom = ("face", face_ms, face_bytes) if face_ms >= cell_ms else ("cell", cell_ms, cell_bytes)
+    achieved = dom[2] / (dom[1] / 1e3) / 1e9
+    step_bytes = 116 * C + 128 * E
+    traffic = None
+    prof = ROOT / "profiles" / "traffic.json"
+    if prof.exists():
+        try:
+            traffic = json.loads(prof.read_text()).get(dom[0])
+        except Exception:
+            traffic = None
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
+           "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": workload_config(args.config, sc, mesh, world,
+                                     {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
+                                      "device_bytes": solver.memory_bytes()}),
+           "gpu_launches": 3 * K + 1,
+           "gpu_launches_note": "1 graph launch = gate kernel + K x (face, cell, finalize) "
+                                f"(host-side launch calls: {launches})",
+           "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+                        "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                        "peak_source": peak_src,
+                        "algorithmic_bytes_per_launch": dom[2],
+                        "kernel_ms": {"face": face_ms, "cell": cell_ms, "finalize": fin_ms},
+                        "step": {"algorithmic_bytes": step_bytes,
+                                 "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
+                                 "frac": step_bytes / (ms / K / 1e3) / 1e9 / peak}},
+           "clocks": clk.summary()}
+
+    if not args.no_e2e:
+        out["e2e"] = e2e_run(api, solver, sc, K, horizon, torch)
+    if rank == 0 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(sc, mesh, args)
+    if rank == 0:
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_run(api, solver, sc, K, horizon, torch):
+    """Public C-ABI with pinned host buffers: H2D state, K steps with per-step
+    stats records back to the host, D2H final state."""
+    C = solver.n_cells
+    pin = [torch.empty(C, dtype=torch.float64).pin_memory() for _ in range(6)]
+    for dst, src in zip(pin[:3], (sc.state.h, sc.state.qx, sc.state.qy)):
+        dst.numpy()[:] = src
+    ptrs_in = [p.data_ptr() for p in pin[:3]]
+    ptrs_out = [p.data_ptr() for p in pin[3:]]
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    solver.set_state_ptrs(*ptrs_in, t=0.0, step=0)
+    recs = solver.advance(t_end=horizon, max_steps=K)
+    solver.get_state_ptrs(*ptrs_out)
+    el = time.perf_counter() - t0
+    assert len(recs) == K
+    h2d, d2h = 24 * C, 24 * C + 40 * K
+    return {"value": C * K / el, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
+            "d2h_bytes_per_step": d2h / K, "wall_s": el,
+            "path": "swe_dev_set_state (pinned H2D) + swe_dev_advance (K steps, stats rows D2H) + "
+                    "swe_dev_get_state (pinned D2H), host wall clock"}
+
+
+def cpu_baseline(sc, mesh, args):
+    from oracle.pyoracle import RefOracle
+    if not RefOracle.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "unavailable: oracle/_ref not built"}
+    threads = reference_threads()
+    # size the sample to ~cpu_seconds of work at ~5e7 cell-updates/s/8 threads
+    est = 6e6 * threads
+    steps = int(max(2, min(50, args.cpu_seconds * est / mesh.n_cells)))
+    value, phase_s, setup_s = time_reference(sc, mesh, steps, 1, threads)
+    return {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"{steps} steps of the full {mesh.n_cells}-cell workload after 1 warm-up "
+                      f"step ({phase_s:.1f} s of phase time, reference build_mesh {setup_s:.1f} s "
+                      f"excluded), {threads} OpenMP threads"}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()

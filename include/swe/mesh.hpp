@@ -94,16 +94,17 @@ inline int rotated_cell_index(int c, int nx, int ny) {
 }
 
 /// Unstructured variant of the square grid: interior nodes
-/// jittered by U(-jitter, +jitter) grid spacings, each square split along a
+/// jittered by U(-jitter, +jitter) grid spacings (jitter < 0.25 keeps every
+/// triangle positive for either diagonal; SURVEY's 0.3 can invert them), each square split along a
 /// random diagonal, then node and cell numbering randomly permuted and each
 /// triangle's vertex list randomly rotated/reflected.  Deterministic in seed.
-inline RawMesh generate_unstructured_mesh(int nx, int ny, double lx, double ly, double jitter = 0.3,
+inline RawMesh generate_unstructured_mesh(int nx, int ny, double lx, double ly, double jitter = 0.2,
                                           std::uint64_t seed = 1807) {
   if (nx < 1 || ny < 1) throw mesh_error("generate_unstructured_mesh: nx and ny must be >= 1");
   if (!(lx > 0.0) || !(ly > 0.0))
     throw mesh_error("generate_unstructured_mesh: Lx and Ly must be > 0");
-  if (!(jitter >= 0.0) || !(jitter < 0.5))
-    throw mesh_error("generate_unstructured_mesh: jitter must lie in [0, 0.5)");
+  if (!(jitter >= 0.0) || !(jitter < 0.25))
+    throw mesh_error("generate_unstructured_mesh: jitter must lie in [0, 0.25)");
   std::mt19937_64 rng(seed);
   auto unit = [&rng]() { return double(rng() >> 11) * 0x1.0p-53; };  // [0,1)
   const double dx = lx / nx, dy = ly / ny;

@@ -136,7 +136,7 @@ def generate_square_mesh(nx: int, ny: int, lx: float, ly: float) -> RawMesh:
     return RawMesh(h)
 
 
-def generate_unstructured_mesh(nx, ny, lx, ly, jitter=0.3, seed=1807) -> RawMesh:
+def generate_unstructured_mesh(nx, ny, lx, ly, jitter=0.2, seed=1807) -> RawMesh:
     err = _errbuf()
     h = L.load().swe_host_raw_unstructured(nx, ny, lx, ly, jitter, seed, err, len(err))
     if not h:
