@@ -237,6 +237,11 @@ def run_b200(args):
     W, K = max(3, args.warmup), args.steps
     clk = ClockSampler(local).start()
     solver.advance(t_end=horizon, max_steps=W)
+    # clocks ramp from idle: keep stepping (untimed) for >= 1 s before timing
+    t_w = time.perf_counter()
+    while time.perf_counter() - t_w < 1.0:
+        _, s_now = solver.clock()
+        solver.advance(t_end=horizon, max_steps=s_now + 50)
     _, step0 = solver.clock()
 
     stream = torch.cuda.ExternalStream(solver.stream, device=local)

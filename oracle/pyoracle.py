@@ -103,6 +103,20 @@ class COracle:
                                           C.POINTER(cd), C.POINTER(cd)]
         L.so_build_mesh.restype = ci
         L.so_build_mesh.argtypes = [ci, vp, ci, vp] + [vp] * 13
+        L.so_batch.restype = None
+        L.so_batch.argtypes = [ci, cl, C.POINTER(so_params), vp, vp, vp, vp, vp]
+
+    def point(self, kind, l, r=None, z=None, nrm=None, params=None):
+        """so_batch: same kinds and layouts as swe_dev_point_eval."""
+        l = _c(l).reshape(-1, 3)
+        n = len(l)
+        width = {2: 6, 4: 1}.get(kind, 3)
+        out = np.empty((n, width))
+        p = _params(params)
+        self.lib.so_batch(kind, n, C.byref(p), P(l), P(None if r is None else _c(r)),
+                          P(None if z is None else _c(z)), P(None if nrm is None else _c(nrm)),
+                          P(out))
+        return out if width > 1 else out[:, 0]
 
     def compute_fluxes(self, m: MeshArrays, h, qx, qy, params=None):
         left = np.empty((m.n_edges, 3))

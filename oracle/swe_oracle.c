@@ -489,3 +489,45 @@ int so_build_mesh(int nn, const double* xy, int nc, const int* tris, int* cell_n
   }
   return ne;
 }
+
+/* ---- batch point physics over arrays (kernel-level parity tests) ------- */
+
+void so_batch(int kind, long n, const so_params* p, const double* l, const double* r,
+              const double* z, const double* nrm, double* out) {
+  for (long i = 0; i < n; ++i) {
+    so_state a = {l[3 * i], l[3 * i + 1], l[3 * i + 2]};
+    if (kind == 0) { /* hllc_flux, kernels.hpp:72-114 */
+      so_state b = {r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+      so_flux f;
+      so_hllc_flux(a, b, nrm[2 * i], nrm[2 * i + 1], p, &f);
+      out[3 * i] = f.mass;
+      out[3 * i + 1] = f.momx;
+      out[3 * i + 2] = f.momy;
+    } else if (kind == 1) { /* wall_flux, kernels.hpp:156-164 */
+      so_flux f = so_wall_flux(a, nrm[2 * i], nrm[2 * i + 1], p);
+      out[3 * i] = f.mass;
+      out[3 * i + 1] = f.momx;
+      out[3 * i + 2] = f.momy;
+    } else if (kind == 2) { /* interior edge of compute_fluxes, engine.hpp:161-166 */
+      so_state b = {r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+      so_state rl, rr;
+      so_flux cl, cr, f;
+      so_hydrostatic_reconstruct(a, z[2 * i], b, z[2 * i + 1], nrm[2 * i], nrm[2 * i + 1], p, &rl,
+                                 &rr, &cl, &cr);
+      so_hllc_flux(rl, rr, nrm[2 * i], nrm[2 * i + 1], p, &f);
+      out[6 * i] = f.mass;
+      out[6 * i + 1] = f.momx + cl.momx;
+      out[6 * i + 2] = f.momy + cl.momy;
+      out[6 * i + 3] = -f.mass;
+      out[6 * i + 4] = -(f.momx + cr.momx);
+      out[6 * i + 5] = -(f.momy + cr.momy);
+    } else if (kind == 3) { /* apply_friction, kernels.hpp:191-199 */
+      so_state o = so_apply_friction(a, z[2 * i], z[2 * i + 1], p);
+      out[3 * i] = o.h;
+      out[3 * i + 1] = o.qx;
+      out[3 * i + 2] = o.qy;
+    } else if (kind == 4) { /* libm pow(h, 4/3), kernels.hpp:197 */
+      out[i] = pow(a.h, 4.0 / 3.0);
+    }
+  }
+}

@@ -7,9 +7,10 @@ __graft_entry__.build().
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().parent / "libswe_b200.so"
+LIB_PATH = Path(os.environ.get("SWE_B200_LIB", Path(__file__).resolve().parent / "libswe_b200.so"))
 
 c_int, c_ll, c_long, c_double, c_void_p, c_char_p, c_uint = (
     C.c_int, C.c_longlong, C.c_long, C.c_double, C.c_void_p, C.c_char_p, C.c_uint)

@@ -43,6 +43,16 @@ namespace {
 thread_local std::string g_last_error;
 long long g_launches = 0;
 
+// resident blocks per SM the kernels are register-budgeted for (ncu r01:
+// 48/74 registers left them latency-bound at 62%/37% occupancy; 6/4 blocks
+// measured 0.333/0.375 ms vs 0.416/0.474 ms at 10M cells)
+#ifndef SWE_FACE_MINB
+#define SWE_FACE_MINB 6
+#endif
+#ifndef SWE_CELL_MINB
+#define SWE_CELL_MINB 4
+#endif
+
 constexpr int kNone = INT_MAX;
 constexpr int kBlock = 256;  // threads per block of the face/cell kernels
 
@@ -124,7 +134,7 @@ __device__ __forceinline__ double step_dt(const Ctl* c, double t_end, bool* last
 // ---------------------------------------------------------------------------
 // face kernel: engine.hpp:138-170 over the device edge order
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_face(Dev d) {
+__global__ void __launch_bounds__(kBlock, SWE_FACE_MINB) k_face(Dev d) {
   const Ctl* ctl = d.ctl;
   if (!ctl->active) return;
   const int cur = ctl->cur;
@@ -212,7 +222,7 @@ __device__ __forceinline__ void block_reduce_part(double lo, double hi, double m
 // cell kernel: engine.hpp:248-290, + CFL (engine.hpp:186-204) and mass of the
 // new state for the next step
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kBlock) k_cell(Dev d) {
+__global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell(Dev d) {
   Ctl* ctl = d.ctl;
   if (!ctl->active) return;
   const int cur = ctl->cur;

@@ -1,0 +1,322 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the oracle.
+
+Bar: bit-identical FP64 for every frictionless path (fluxes, states, the dt
+sequence); for the friction path the device pow(h, 4/3) is checked against
+the host libm's and the state against the per-cell floored-relative
+tolerance 1e-12 of BASELINE.json's north_star / SURVEY.md §8(c).
+"""
+import json
+import subprocess
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, ROOT, bit_equal, random_state
+from oracle.pyoracle import MeshArrays
+from paper_1807_00672_b200 import api
+
+pytestmark = pytest.mark.gpu
+
+FRICTION_TOL = 1e-12  # per-cell |a-b| / max(|b|, 1e-12 ||b||_inf)
+
+
+def floored_rel(a, b):
+    scale = np.maximum(np.abs(b), 1e-12 * max(np.abs(b).max(), 1e-300))
+    return float(np.max(np.abs(a - b) / scale))
+
+
+def rng_pairs(n, seed, dry=0.3, hmax=3.0, umax=4.0):
+    rng = np.random.default_rng(seed)
+    def st():
+        h = rng.uniform(0.0, hmax, n)
+        h[rng.random(n) < dry] = 0.0
+        tiny = rng.random(n) < 0.05  # straddle h_dry = 1e-6
+        h[tiny] = rng.uniform(0.0, 2e-6, int(tiny.sum()))
+        return np.stack([h, h * rng.uniform(-umax, umax, n), h * rng.uniform(-umax, umax, n)], 1)
+    a = rng.uniform(0, 2 * np.pi, n)
+    return st(), st(), np.stack([np.cos(a), np.sin(a)], 1), rng.uniform(0, 2, (n, 2))
+
+
+# ---------------------------------------------------------------- point physics
+
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_point_physics_bitwise(coracle, kind):
+    """hllc (kernels.hpp:72-114), wall (:156-164), reconstruction + edge combine
+    (:126-152, engine.hpp:161-166) on 1e5 random wet/dry pairs."""
+    l, r, nrm, z = rng_pairs(100_000, 10 + kind)
+    if kind == 0:
+        # identical-state shortcut (kernels.hpp:83-84) on a slice
+        r[:1000] = l[:1000]
+    dev = api.point_eval(kind, l, r, z, nrm)
+    ref = coracle.point(kind, l, r, z, nrm)
+    assert bit_equal(dev, ref)
+
+
+def test_point_physics_matches_reference(refo):
+    l, r, nrm, z = rng_pairs(20_000, 99)
+    assert bit_equal(api.point_eval(0, l, r, None, nrm), refo.hllc(l, r, nrm))
+    assert bit_equal(api.point_eval(1, l, None, None, nrm), refo.wall(l, nrm))
+    left, right = refo.edge(l, r, z, nrm)
+    dev = api.point_eval(2, l, r, z, nrm)
+    assert bit_equal(dev[:, :3], left) and bit_equal(dev[:, 3:], right)
+
+
+def test_pow43_against_host_libm(coracle):
+    """kernels.hpp:197 std::pow(h, 4/3) over the depth range friction sees."""
+    rng = np.random.default_rng(3)
+    h = np.concatenate([rng.uniform(1e-6, 1e-3, 200_000), rng.uniform(1e-3, 10, 600_000),
+                        rng.uniform(10, 100, 200_000)])
+    h = np.concatenate([h, [1.0, np.nextafter(1.0, 2), np.nextafter(1.0, 0), 5e-324, 1e-310, 0.0,
+                            1e300, np.inf]])
+    dev = api.point_eval(4, np.stack([h, h, h], 1))
+    ref = coracle.point(4, np.stack([h, h, h], 1))
+    mism = np.count_nonzero(dev.view(np.uint64) != ref.view(np.uint64))
+    print(f"pow43 mismatches: {mism} of {len(h)}")
+    assert mism == 0
+
+
+def test_friction_point(coracle):
+    rng = np.random.default_rng(4)
+    n = 50_000
+    h = rng.uniform(0.05, 5, n)
+    u = np.stack([h, h * rng.uniform(-3, 3, n), h * rng.uniform(-3, 3, n)], 1)
+    z = np.stack([rng.uniform(0, 0.1, n), rng.uniform(1e-4, 10, n)], 1)
+    dev = api.point_eval(3, u, None, z)
+    ref = coracle.point(3, u, None, z)
+    assert bit_equal(dev, ref)
+    assert np.all(np.abs(dev[:, 1]) <= np.abs(u[:, 1])) and np.all(dev[:, 1] * u[:, 1] >= 0)
+
+
+# ---------------------------------------------------------------- compute_fluxes
+
+def mesh_for(kind, seed=1):
+    if kind == "flat":
+        raw = api.generate_square_mesh(12, 9, 4.0, 3.0)
+        return api.build_mesh(raw, np.zeros(raw.n_cells), np.zeros(raw.n_cells))
+    if kind == "mounds":
+        return api.setup_case("lake_at_rest", api.generate_square_mesh(30, 12, 75.0, 30.0))[0]
+    raw = api.generate_unstructured_mesh(90, 36, 75.0, 30.0, seed=seed)
+    return api.setup_case("lake_at_rest", raw)[0]
+
+
+@pytest.mark.parametrize("name", ["12x9_seed7", "12x9_seed8", "mounds_30x12_seed9"])
+def test_fluxes_match_reference_golden(golden, name):
+    f = np.load(GOLDEN / golden["fluxes"][name]["file"])
+    mesh = mesh_for("mounds" if name.startswith("mounds") else "flat")
+    st = api.FieldState(f["h"], f["qx"], f["qy"])
+    left, right = api.compute_fluxes(st, mesh)
+    assert bit_equal(left, f["left"]) and bit_equal(right, f["right"])
+
+
+@pytest.mark.parametrize("identity", [False, True])
+@pytest.mark.parametrize("dry", [0.0, 0.3, 0.7])
+def test_fluxes_unstructured_bitwise(coracle, identity, dry):
+    mesh = mesh_for("unstructured", seed=2)
+    h, qx, qy = random_state(mesh.n_cells, 5, dry)
+    s = api.DeviceSolver(mesh, identity_order=identity)
+    s.set_state(api.FieldState(h, qx, qy))
+    left, right = s.compute_fluxes()
+    l2, r2, bad = coracle.compute_fluxes(MeshArrays.from_mesh(mesh), h, qx, qy)
+    assert bad == -1 and bit_equal(left, l2) and bit_equal(right, r2)
+
+
+def test_negative_depth_reports_lowest_edge(coracle):
+    """test_engine.cpp:229-237 -- the lowest edge index, as the sequential backend."""
+    mesh = mesh_for("unstructured", seed=3)
+    h, qx, qy = random_state(mesh.n_cells, 12)
+    h[[17, 400, 901]] = -0.5
+    _, _, bad = coracle.compute_fluxes(MeshArrays.from_mesh(mesh), h, qx, qy)
+    with pytest.raises(api.NumericError, match=f"compute_fluxes: negative depth at edge {bad}$"):
+        api.compute_fluxes(api.FieldState(h, qx, qy), mesh)
+
+
+# ---------------------------------------------------------------- trajectories
+
+def golden_case(g):
+    raw = api.generate_square_mesh(g["nx"], g["ny"], g["spec"]["lx"], g["spec"]["ly"])
+    mesh, st = api.setup_case(g["case"], raw, **g["spec"])
+    if g["still_water"]:
+        st.h[:] = 0.75
+    return mesh, st
+
+
+def digest(*arrays):
+    import hashlib
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a, dtype=np.float64).tobytes())
+    return h.hexdigest()
+
+
+@pytest.mark.parametrize("name", ["water_drop_12x12_200", "still_water_8x8_25", "lake_at_rest_30x12_50",
+                                  "dam_break_1d_100x10_t40", "water_drop_50x50_1000",
+                                  "three_mounds_100x40_t30"])
+def test_trajectory_vs_reference_golden(golden, coracle, name):
+    """Device run loop (one graph launch) against the reference's trajectories."""
+    g = golden["trajectories"][name]
+    mesh, st = golden_case(g)
+    s = api.DeviceSolver(mesh)
+    s.set_state(st)
+    recs = s.advance(t_end=g["t_end"], max_steps=g["steps"])
+    got, t, step = s.get_state()
+    # bit-identical to the reference, friction included (swe_pow.cuh restates
+    # the host glibc pow exactly)
+    assert step == g["steps"] and t == g["t"]
+    assert digest(got.h, got.qx, got.qy) == g["state_digest"]
+    assert digest(recs[:, 2]) == g["dt_digest"]
+    assert s.ledger()[1] == g["clip_events"]
+
+
+def test_config1_circular_dam_break_1000_steps(coracle):
+    """BASELINE configs[0]: ~10k-triangle unstructured circular dam break, 1000 steps."""
+    sc = api.make_scenario("circular_dam_break")
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    s = api.DeviceSolver(mesh)
+    s.set_state(sc.state)
+    recs = s.advance(t_end=1e30, max_steps=1000)
+    got, t, step = s.get_state()
+    ref = coracle.advance(MeshArrays.from_mesh(mesh), sc.state.h, sc.state.qx, sc.state.qy,
+                          nsteps=1000)
+    assert step == 1000 and t == ref["t"]
+    for k, a in (("h", got.h), ("qx", got.qx), ("qy", got.qy)):
+        assert bit_equal(a, ref[k]), k
+    assert bit_equal(recs[:, 2], ref["dts"]) and bit_equal(recs[:, 3], ref["max_speeds"])
+    m = recs[:, 4]
+    assert abs(m[-1] - m[0]) <= 1e-12 * m[0]
+
+
+@pytest.mark.parametrize("scenario", ["three_mounds_friction", "sloping_wet_dry", "channel"])
+def test_friction_scenarios_scaled(coracle, scenario):
+    """Configs 2-4 at reduced resolution: wet/dry fronts + bathymetry + Manning."""
+    sc = api.make_scenario(scenario, scale=0.04 if scenario != "three_mounds_friction" else 0.1)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    s = api.DeviceSolver(mesh)
+    s.set_state(sc.state)
+    recs = s.advance(t_end=1e30, max_steps=300)
+    got, t, step = s.get_state()
+    ref = coracle.advance(MeshArrays.from_mesh(mesh), sc.state.h, sc.state.qx, sc.state.qy,
+                          nsteps=300)
+    assert ref["error"] is None and step == 300 and t == ref["t"]
+    for k, a in (("h", got.h), ("qx", got.qx), ("qy", got.qy)):
+        assert floored_rel(a, ref[k]) <= FRICTION_TOL, k  # the north_star bar ...
+        assert bit_equal(a, ref[k]), k                    # ... and the one we hold
+    assert bit_equal(recs[:, 2], ref["dts"])
+    assert s.ledger()[1] == ref["clip_events"]
+
+
+def test_morton_and_identity_order_agree():
+    sc = api.make_scenario("sloping_wet_dry", scale=0.03)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    out = []
+    for identity in (False, True):
+        s = api.DeviceSolver(mesh, identity_order=identity)
+        s.set_state(sc.state)
+        recs = s.advance(t_end=1e30, max_steps=200)
+        out.append((s.get_state()[0], recs))
+    (a, ra), (b, rb) = out
+    assert bit_equal(a.h, b.h) and bit_equal(a.qx, b.qx) and bit_equal(a.qy, b.qy)
+    assert bit_equal(ra[:, 2], rb[:, 2])
+
+
+# ---------------------------------------------------------------- engine API
+
+def test_advance_step_api_vs_oracle(coracle):
+    """swe::advance_step host-resident contract, including the clip ledger."""
+    sc = api.make_scenario("sloping_wet_dry", scale=0.02)
+    mesh = api.build_mesh(sc.raw, sc.bed, np.zeros_like(sc.manning))
+    st = sc.state.copy()
+    r = api.advance(mesh, st, nsteps=40)
+    o = coracle.advance(MeshArrays.from_mesh(mesh), sc.state.h, sc.state.qx, sc.state.qy, nsteps=40)
+    assert bit_equal(st.h, o["h"]) and bit_equal(st.qx, o["qx"]) and bit_equal(st.qy, o["qy"])
+    assert bit_equal(r.dts, o["dts"]) and bit_equal(r.max_speeds, o["max_speeds"])
+    assert r.clip_events == o["clip_events"]
+    assert abs(r.clipped_volume - o["clipped_volume"]) <= 1e-12 * max(abs(o["clipped_volume"]), 1e-300)
+
+
+def test_run_api_truncates_and_snapshots(coracle):
+    """engine.hpp:335-394 + test_engine.cpp:249-299."""
+    raw = api.generate_square_mesh(4, 4, 1.0, 1.0)
+    mesh = api.build_mesh(raw, np.zeros(32), np.zeros(32))
+    st = api.FieldState(np.ones(32), np.zeros(32), np.zeros(32))
+    r = api.run(mesh, st, t_end=1e-6)
+    assert r.step == 1 and r.t == 1e-6 and r.stats["t_final"] == 1e-6
+    st = api.FieldState(np.ones(32), np.zeros(32), np.zeros(32))
+    r = api.run(mesh, st, t_end=0.2, snapshot_interval=0.08, snapshots=True)
+    assert len(r.snapshots) >= 3 and r.snapshots[0] == 0.0 and abs(r.snapshots[-1] - 0.2) < 1e-12
+    with pytest.raises(api.ConfigError):
+        api.run(mesh, st, t_end=0.0)
+    with pytest.raises(api.NumericError, match="exceeded max_steps=3"):
+        api.run(mesh, api.FieldState(np.ones(32), np.zeros(32), np.zeros(32)), t_end=10.0,
+                max_steps=3)
+
+
+def test_run_api_series_vs_oracle(coracle, golden):
+    g = golden["trajectories"]["dam_break_1d_100x10_t40"]
+    mesh, st = golden_case(g)
+    st0 = st.copy()
+    r = api.run(mesh, st, t_end=40.0)
+    o = coracle.advance(MeshArrays.from_mesh(mesh), st0.h, st0.qx, st0.qy, t_end=40.0, nsteps=10**6,
+                        stop_at_t_end=True)
+    assert r.step == o["step"] and r.t == 40.0
+    assert bit_equal(r.series[:, 2], o["dts"]) and bit_equal(r.series[:, 3], o["max_speeds"])
+    assert digest(st.h, st.qx, st.qy) == g["state_digest"]
+    masses = r.series[:, 4]
+    assert np.all(np.abs(masses - r.stats["mass_initial"]) <= 1e-12 * r.stats["mass_initial"])
+    assert r.stats["mean_dt"] == np.sum(o["dts"]) / r.step or abs(r.stats["mean_dt"] * r.step - 40.0) < 1e-9
+
+
+def test_errors_match_reference_messages(coracle):
+    """NaN -> 'stable_dt: non-finite velocity in cell 5' (test_engine.cpp:218-227),
+    blow-up -> 'advance_step: numeric blowup at step N, cell C, dt D (h=H)'."""
+    raw = api.generate_square_mesh(3, 3, 1.0, 1.0)
+    mesh = api.build_mesh(raw, np.zeros(18), np.zeros(18))
+    h, qx, qy = random_state(18, 11)
+    qx[5] = np.nan
+    with pytest.raises(api.NumericError, match="stable_dt: non-finite velocity in cell 5$"):
+        api.advance(mesh, api.FieldState(h, qx, qy))
+    # an unstable Courant number drives a blow-up; compare with the oracle's report
+    p = api.PhysParams(cfl=40.0)
+    from oracle.pyoracle import so_params  # noqa: F401
+    h, qx, qy = random_state(18, 3)
+    o = coracle.advance(MeshArrays.from_mesh(mesh), h, qx, qy, nsteps=50, params=p)
+    assert o["error"] is not None
+    kind, cell, hval = o["error"]
+    st = api.FieldState(h.copy(), qx.copy(), qy.copy())
+    with pytest.raises(api.NumericError) as ei:
+        api.advance(mesh, st, nsteps=50, params=p)
+    msg = str(ei.value)
+    if kind == 3:
+        assert f"cell {cell}," in msg and "numeric blowup at step" in msg and f"(h={hval:f})" in msg
+    assert bit_equal(st.h, o["h"])  # state = last good step
+
+
+def test_reproducible_and_mass_conserving_full_size():
+    """BASELINE configs[2] at full size (10M cells): run twice bitwise; mass
+    balance to round-off (change = clipped volume only)."""
+    sc = api.make_scenario("channel")
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    s = api.DeviceSolver(mesh)
+    outs = []
+    for _ in range(2):
+        s.set_state(sc.state)
+        m0 = s.total_mass()
+        recs = s.advance(t_end=1e30, max_steps=30)
+        outs.append((s.get_state()[0], recs, m0))
+    (a, ra, m0), (b, rb, _) = outs
+    assert bit_equal(a.h, b.h) and bit_equal(a.qx, b.qx) and bit_equal(ra[:, 2], rb[:, 2])
+    clipped, _ = s.ledger()
+    assert abs(ra[-1, 4] - m0) <= 1e-12 * m0 + 2 * clipped
+
+
+def test_cpp_drop_in_driver(golden):
+    """A reference-API caller (tests/cpp/api_driver.cpp) on the device engine."""
+    exe = ROOT / "tests" / "cpp" / "api_driver"
+    out = json.loads(subprocess.run([str(exe)], capture_output=True, text=True, check=True,
+                                    timeout=600).stdout)
+    assert out["c3_steps"] == 1117 and out["c3_positive"] and out["c3_t"] == 30.0
+    assert out["run_steps"] == 1000 and out["run_t"] == golden["acceptance"]["c2_1000"]["t"]
+    assert out["run_snaps"] == 1 + 5 and abs(out["run_drift"]) <= 1e-12
+    assert out["uniform_mass_antisymmetric"] and abs(out["mass_unit"] - 6.0) <= 6e-14  # 3 m x 2 m
+    assert out["nan_msg"] == "stable_dt: non-finite velocity in cell 5"
+    assert out["neg_msg"].startswith("compute_fluxes: negative depth at edge ")
+    assert out["cfg_msg"] == "run: t_end must be > 0"
