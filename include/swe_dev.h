@@ -88,6 +88,8 @@ typedef struct {
 /* create flags */
 #define SWE_FLAG_IDENTITY_ORDER 1u /* skip the Morton renumbering */
 #define SWE_FLAG_NO_GRAPH 2u       /* advance with plain launches, no CUDA graph */
+#define SWE_FLAG_TWO_PHASE 4u      /* face kernel + cell kernel (records through HBM)
+                                      instead of the fused tile kernel */
 
 /* Uploads the mesh, renumbers it on the device, allocates the double-buffered
  * state and edge records.  device = CUDA ordinal. */
@@ -141,6 +143,11 @@ SWE_API int swe_dev_total_mass(swe_dev_ctx* ctx, double* mass);
  * kernel (ms): [0] face, [1] cell, [2] finalize, [3] cfl. */
 SWE_API int swe_dev_set_profiling(swe_dev_ctx* ctx, int on);
 SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launches, int n);
+
+/* Layout facts: [0] fused?, [1] cells per tile, [2] tiles, [3] max slots per
+ * tile, [4] halo edges, [5] tile grid, [6] face grid, [7] cell grid,
+ * [8] tile shared-memory bytes, [9] edges. */
+SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
 
 /* cudaStream_t of the context (as void*), for events on the launching stream. */
 SWE_API void* swe_dev_stream(swe_dev_ctx* ctx);

@@ -47,6 +47,7 @@ class swe_step_record(C.Structure):
 SWE_OK, SWE_NONFINITE_SPEED, SWE_NEGATIVE_DEPTH, SWE_BLOWUP, SWE_CUDA, SWE_NCCL, SWE_INVALID = range(7)
 SWE_FLAG_IDENTITY_ORDER = 1
 SWE_FLAG_NO_GRAPH = 2
+SWE_FLAG_TWO_PHASE = 4
 
 _SIGS = {
     # device solver (swe_dev.h)
@@ -68,6 +69,7 @@ _SIGS = {
     "swe_dev_total_mass": (c_int, [c_void_p, P_double]),
     "swe_dev_set_profiling": (c_int, [c_void_p, c_int]),
     "swe_dev_kernel_times": (c_int, [c_void_p, P_double, P_ll, c_int]),
+    "swe_dev_info": (c_int, [c_void_p, P_ll, c_int]),
     "swe_dev_stream": (c_void_p, [c_void_p]),
     "swe_dev_memory_bytes": (c_ll, [c_void_p]),
     "swe_dev_launch_count": (c_ll, []),

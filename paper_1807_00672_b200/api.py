@@ -411,14 +411,16 @@ class DeviceSolver:
     """swe_dev_ctx: mesh + double-buffered state resident on one B200."""
 
     def __init__(self, mesh: Mesh, params: PhysParams = PhysParams(), device: int = 0,
-                 identity_order: bool = False, graph: bool = True):
+                 identity_order: bool = False, graph: bool = True, two_phase: bool = False):
         self.lib = L.load()
         self.mesh = mesh
         self.params = params
         v = mesh.view()
         p = params.c()
         ctx = C.c_void_p()
-        flags = (L.SWE_FLAG_IDENTITY_ORDER if identity_order else 0) | (0 if graph else L.SWE_FLAG_NO_GRAPH)
+        flags = ((L.SWE_FLAG_IDENTITY_ORDER if identity_order else 0)
+                 | (0 if graph else L.SWE_FLAG_NO_GRAPH)
+                 | (L.SWE_FLAG_TWO_PHASE if two_phase else 0))
         _check(self.lib.swe_dev_create(C.byref(v), C.byref(p), device, flags, C.byref(ctx)),
                "swe_dev_create")
         self.ctx = ctx
@@ -511,8 +513,16 @@ class DeviceSolver:
         ms = (C.c_double * 4)()
         n = (C.c_longlong * 4)()
         _check(self.lib.swe_dev_kernel_times(self.ctx, ms, n, 4), "kernel_times")
-        names = ("face", "cell", "finalize", "cfl")
+        names = ("tile", "cell", "finalize", "cfl") if self.info()["fused"] else \
+            ("face", "cell", "finalize", "cfl")
         return {k: (ms[i], n[i]) for i, k in enumerate(names)}
+
+    def info(self) -> dict:
+        v = (C.c_longlong * 10)()
+        _check(self.lib.swe_dev_info(self.ctx, v, 10), "swe_dev_info")
+        keys = ("fused", "tile_cells", "tiles", "max_slots", "halo_edges", "grid_tile",
+                "grid_face", "grid_cell", "tile_smem_bytes", "edges")
+        return dict(zip(keys, list(v)))
 
     @property
     def stream(self) -> int:

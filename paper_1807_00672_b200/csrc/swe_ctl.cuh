@@ -1,0 +1,287 @@
+// swe_ctl.cuh -- device control block, launch-sequence kernels and the
+// fixed-order reductions of the explicit step (engine.hpp:179-216, :226-319,
+// :355-380).  Included by swe_dev.cu only.
+#pragma once
+
+#include <climits>
+
+#include "swe_dev.h"
+#include "swe_phys.cuh"
+
+namespace swe_b200 {
+
+constexpr int kNone = INT_MAX;  // "no error index"
+constexpr int kBlock = 256;     // threads per block of the step kernels
+
+struct StepParams {  // written by the host before a launch sequence
+  double t_end;
+  long long max_steps;
+  double next_snap;
+  long long rec_cap;
+  int ring;  // records wrap instead of stopping the loop
+  int mode;  // 0 run loop, 1 single advance_step (no t/max_steps gate), 2 flux only
+};
+
+struct Ctl {
+  // committed clock and ledger
+  double t;
+  long long step;
+  double clipped;
+  long long events;
+  // CFL cache of the current state
+  double dts;        // cfl * min(r / speed), or dt_max when all dry
+  double max_speed;  // of the current state
+  double mass;       // of the current state (fixed-order tree sum)
+  int cfl_valid;
+  int cfl_bad;  // lowest reference cell with a non-finite speed, or kNone
+  // loop state
+  int cur;     // which buffer holds the current state
+  int active;  // kernels run only when set
+  long long n_rec;
+  // outcome
+  int status;
+  int err_index;
+  long long err_step;
+  double err_dt;
+  double err_h;
+  // per-step error scratch (lowest reference index, kNone = none)
+  int bad_edge;
+  int bad_cell;
+  int bad_speed;
+  int pad;
+};
+
+struct Part {  // one block's partial results
+  double lo, hi, mass, clip;
+  long long events;
+  long long pad;
+};
+
+struct Dev {
+  int C, E;
+  // cells (device order)
+  const double *area, *inr, *z, *man;
+  const int *inc0, *inc1, *inc2;  // (device edge << 1) | (sign < 0), reference local order
+  const int* c_orig;              // device cell -> reference cell
+  const int* c_new;               // reference cell -> device cell
+  // edges (device order: owner tile, walls last within a tile, lower cell)
+  const int *el, *er;  // er < 0: reflective wall
+  const double *nx, *ny, *len;
+  const int* e_orig;
+  // tiles of T consecutive cells (fused path)
+  int T, ntiles, max_slots;
+  const int* eoff;       // [ntiles+1] owned edge range of each tile
+  const int* hoff;       // [ntiles+1] halo list range of each tile
+  const int* halo;       // halo edges (owned by another tile, touching this one)
+  const ushort4* slots;  // per cell: (tile-local slot << 1) | (sign < 0), x3
+  // state, double-buffered
+  double *h[2], *qx[2], *qy[2];
+  // edge records of the two-phase path
+  double *M, *LX, *LY, *RX, *RY;
+  // control
+  Ctl* ctl;
+  const StepParams* sp;
+  Part* part;
+  swe_step_record* rec;
+  Phys P;
+};
+
+// engine.hpp:236-237
+__device__ __forceinline__ double step_dt(const Ctl* c, double t_end, bool* last_out) {
+  const bool last = c->t + c->dts >= t_end;
+  if (last_out) *last_out = last;
+  return last ? t_end - c->t : c->dts;
+}
+
+// block reduction of per-thread partials in a fixed tree order
+__device__ __forceinline__ void block_reduce_part(double lo, double hi, double mass, double clip,
+                                                  long long ev, Part* out) {
+  __shared__ double s_lo[kBlock / 32], s_hi[kBlock / 32], s_m[kBlock / 32], s_c[kBlock / 32];
+  __shared__ long long s_e[kBlock / 32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    lo = sel_min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = sel_max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    mass += __shfl_xor_sync(0xffffffffu, mass, o);
+    clip += __shfl_xor_sync(0xffffffffu, clip, o);
+    ev += __shfl_xor_sync(0xffffffffu, ev, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    s_lo[w] = lo;
+    s_hi[w] = hi;
+    s_m[w] = mass;
+    s_c[w] = clip;
+    s_e[w] = ev;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    Part p{s_lo[0], s_hi[0], s_m[0], s_c[0], s_e[0], 0};
+    for (int i = 1; i < (int)(blockDim.x / 32); ++i) {
+      p.lo = sel_min(p.lo, s_lo[i]);
+      p.hi = sel_max(p.hi, s_hi[i]);
+      p.mass += s_m[i];
+      p.clip += s_c[i];
+      p.events += s_e[i];
+    }
+    *out = p;
+  }
+}
+
+// standalone CFL + mass of the current state (first step after set_state),
+// engine.hpp:179-216 and :128-132
+__global__ void __launch_bounds__(kBlock) k_cfl(Dev d) {
+  Ctl* ctl = d.ctl;
+  const int cur = ctl->cur;
+  const double* __restrict__ H = d.h[cur];
+  const double* __restrict__ QX = d.qx[cur];
+  const double* __restrict__ QY = d.qy[cur];
+  double lo = INFINITY, hi = 0.0, mass = 0.0;
+  const int stride = gridDim.x * blockDim.x;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C; c += stride) {
+    const Cons u{H[c], QX[c], QY[c]};
+    mass += u.h * __ldg(d.area + c);
+    if (u.h < d.P.h_dry) continue;
+    const double s = signal_speed(u, d.P);
+    if (!isfinite(s)) {
+      atomicMin(&ctl->bad_speed, __ldg(d.c_orig + c));
+      continue;
+    }
+    lo = sel_min(lo, __ldg(d.inr + c) / s);
+    hi = sel_max(hi, s);
+  }
+  block_reduce_part(lo, hi, mass, 0.0, 0, d.part + blockIdx.x);
+}
+
+// fixed-order reduction of n block partials by one block
+__device__ Part reduce_parts(const Dev& d, int n) {
+  __shared__ Part s[kBlock];
+  Part p{INFINITY, 0.0, 0.0, 0.0, 0, 0};
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const Part q = d.part[i];
+    p.lo = sel_min(p.lo, q.lo);
+    p.hi = sel_max(p.hi, q.hi);
+    p.mass += q.mass;
+    p.clip += q.clip;
+    p.events += q.events;
+  }
+  s[threadIdx.x] = p;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      Part a = s[threadIdx.x];
+      const Part b = s[threadIdx.x + o];
+      a.lo = sel_min(a.lo, b.lo);
+      a.hi = sel_max(a.hi, b.hi);
+      a.mass += b.mass;
+      a.clip += b.clip;
+      a.events += b.events;
+      s[threadIdx.x] = a;
+    }
+    __syncthreads();
+  }
+  return s[0];
+}
+
+__device__ __forceinline__ void set_cfl_cache(Ctl* ctl, const Part& p, const Phys& P) {
+  ctl->dts = isfinite(p.lo) ? P.cfl * p.lo : P.dt_max;  // engine.hpp:214
+  ctl->max_speed = p.hi;
+  ctl->mass = p.mass;
+  ctl->cfl_bad = ctl->bad_speed;
+  ctl->bad_speed = kNone;
+  ctl->cfl_valid = 1;
+}
+
+// prepare: reduce k_cfl's n partials into the CFL cache
+__global__ void __launch_bounds__(kBlock) k_prepare(Dev d, int n) {
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x == 0) set_cfl_cache(d.ctl, p, d.P);
+}
+
+// gate: opens a launch sequence (run() loop entry, engine.hpp:355-358)
+__global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
+  Ctl* c = d.ctl;
+  const StepParams* sp = d.sp;
+  c->status = SWE_OK;
+  c->n_rec = 0;
+  c->bad_edge = kNone;
+  c->bad_cell = kNone;
+  c->bad_speed = kNone;
+  int go = sp->mode != 0 ||
+           (c->t < sp->t_end && c->step < sp->max_steps && (sp->ring || sp->rec_cap > 0));
+  if (go && sp->mode != 2 && c->cfl_bad != kNone) {  // stable_dt throws (engine.hpp:205-206)
+    c->status = SWE_NONFINITE_SPEED;
+    c->err_index = c->cfl_bad;
+    go = 0;
+  }
+  c->active = go;
+  if (use_cond) cudaGraphSetConditional(cond, go);
+}
+
+// finalize: engine.hpp:292-307 + the fused CFL cache for the next step;
+// n = number of partials the step kernel wrote
+__global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
+                                                     int use_cond) {
+  Ctl* c = d.ctl;
+  if (!c->active) {
+    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x != 0) return;
+  const StepParams* sp = d.sp;
+  bool last;
+  const double dt = step_dt(c, sp->t_end, &last);
+  int go = 1;
+  if (c->bad_edge != kNone) {  // engine.hpp:168-169
+    c->status = SWE_NEGATIVE_DEPTH;
+    c->err_index = c->bad_edge;
+    go = 0;
+  } else if (c->bad_cell != kNone) {  // engine.hpp:292-297; state is not committed
+    c->status = SWE_BLOWUP;
+    c->err_index = c->bad_cell;
+    c->err_step = c->step;
+    c->err_dt = dt;
+    c->err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
+    go = 0;
+  }
+  if (!go) {
+    c->bad_edge = kNone;
+    c->bad_cell = kNone;
+    c->bad_speed = kNone;
+    c->active = 0;
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  // commit (engine.hpp:300-307)
+  const double max_speed_pre = c->max_speed;
+  c->clipped += p.clip;
+  c->events += p.events;
+  c->cur ^= 1;
+  c->t = last ? sp->t_end : c->t + dt;
+  c->step += 1;
+  const long long slot = sp->ring ? (c->n_rec % sp->rec_cap) : c->n_rec;
+  if (slot < sp->rec_cap) {
+    swe_step_record r;
+    r.step = c->step;
+    r.t = c->t;
+    r.dt = dt;
+    r.max_speed = max_speed_pre;
+    r.mass = p.mass;
+    d.rec[slot] = r;
+  }
+  c->n_rec += 1;
+  set_cfl_cache(c, p, d.P);
+  // continue? (engine.hpp:355-358, :374-375)
+  go = c->t < sp->t_end && c->step < sp->max_steps && !(c->t >= sp->next_snap - 1e-12) &&
+       (sp->ring || c->n_rec < sp->rec_cap);
+  if (go && c->cfl_bad != kNone) {
+    c->status = SWE_NONFINITE_SPEED;
+    c->err_index = c->cfl_bad;
+    go = 0;
+  }
+  c->active = go;
+  if (use_cond) cudaGraphSetConditional(cond, go);
+}
+
+}  // namespace swe_b200

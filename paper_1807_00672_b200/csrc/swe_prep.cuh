@@ -1,0 +1,245 @@
+// swe_prep.cuh -- device mesh preprocessor (run once per swe_dev_create):
+// Morton renumbering of cells, edge ordering by owner tile, the tile tables
+// of the fused kernel, and the reference<->device permutation kernels.
+// The reference layout it consumes is build_mesh's (mesh.hpp:121-240);
+// orientation (left = reference left cell) and each cell's local edge order
+// are preserved so every sum is formed in the reference's order.
+#pragma once
+
+#include "swe_ctl.cuh"
+
+namespace swe_b200 {
+
+__device__ __forceinline__ unsigned spread16(unsigned v) {
+  v &= 0xffffu;
+  v = (v | (v << 8)) & 0x00ff00ffu;
+  v = (v | (v << 4)) & 0x0f0f0f0fu;
+  v = (v | (v << 2)) & 0x33333333u;
+  v = (v | (v << 1)) & 0x55555555u;
+  return v;
+}
+
+// 32-bit Morton code of the centroid on a 65536^2 grid over the bounding box
+__global__ void k_morton(int C, const double* cx, const double* cy, double x0, double y0, double s,
+                         unsigned* key, int* idx) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const double fx = fmin(fmax((cx[c] - x0) * s, 0.0), 65535.0);
+  const double fy = fmin(fmax((cy[c] - y0) * s, 0.0), 65535.0);
+  key[c] = spread16((unsigned)fx) | (spread16((unsigned)fy) << 1);
+  idx[c] = c;
+}
+
+__global__ void k_iota(int n, int* v) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = i;
+}
+
+__global__ void k_invert(int n, const int* p, int* inv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) inv[p[i]] = i;
+}
+
+// edge order key: (owner tile, wall?, lower device cell); the owner tile is
+// the tile of the edge's lower device cell (its only cell for a wall)
+__global__ void k_edge_keys(int E, const int* el, const int* er, const int* c_new, int T,
+                            unsigned long long* key, int* idx) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int l = c_new[el[e]];
+  const int r = er[e] < 0 ? -1 : c_new[er[e]];
+  const int lo = r < 0 ? l : min(l, r);
+  key[e] = ((unsigned long long)(lo / T) << 33) | ((unsigned long long)(r < 0) << 32) |
+           (unsigned long long)lo;
+  idx[e] = e;
+}
+
+template <class V>
+__global__ void k_gather(int n, const int* perm, const V* src, V* dst) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[perm[i]];
+}
+
+__global__ void k_edges_new(int E, const int* e_orig, const int* el, const int* er,
+                            const int* c_new, int* nel, int* ner) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int o = e_orig[e];
+  nel[e] = c_new[el[o]];
+  ner[e] = er[o] < 0 ? -1 : c_new[er[o]];
+}
+
+__global__ void k_inc_new(int C, const int* c_orig, const int* cell_edge, const int* cell_sign,
+                          const int* e_new, int* i0, int* i1, int* i2, int* bad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int o = c_orig[c];
+  int v[3];
+  for (int k = 0; k < 3; ++k) {
+    const int e = cell_edge[3 * (size_t)o + k];
+    const int s = cell_sign[3 * (size_t)o + k];
+    if (s != 1 && s != -1) atomicExch(bad, 1);
+    v[k] = (e_new[e] << 1) | (s < 0 ? 1 : 0);
+  }
+  i0[c] = v[0];
+  i1[c] = v[1];
+  i2[c] = v[2];
+}
+
+__device__ __forceinline__ int owner_tile(const int* el, const int* er, int e, int T) {
+  const int l = el[e], r = er[e];
+  return (r < 0 ? l : min(l, r)) / T;
+}
+
+// eoff[t] = first edge owned by tile t (edges sorted by owner tile)
+__global__ void k_tile_bounds(int E, const int* el, const int* er, int T, int ntiles, int* eoff) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int ow = owner_tile(el, er, e, T);
+  const int prev = e == 0 ? -1 : owner_tile(el, er, e - 1, T);
+  for (int t = prev + 1; t <= ow; ++t) eoff[t] = e;
+  if (e == E - 1)
+    for (int t = ow + 1; t <= ntiles; ++t) eoff[t] = E;
+}
+
+// interior edges crossing a tile boundary -> (tile of the upper cell, edge)
+__global__ void k_halo_keys(int E, const int* el, const int* er, int T, unsigned long long* key,
+                            int* count) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int r = er[e];
+  if (r < 0) return;
+  const int a = el[e] / T, b = r / T;
+  if (a == b) return;
+  const int slot = atomicAdd(count, 1);
+  key[slot] = ((unsigned long long)max(a, b) << 32) | (unsigned)e;
+}
+
+__global__ void k_halo_bounds(int nh, const unsigned long long* key, int ntiles, int* hoff,
+                              int* halo) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nh) return;
+  const int t = (int)(key[j] >> 32);
+  halo[j] = (int)(key[j] & 0xffffffffu);
+  const int prev = j == 0 ? -1 : (int)(key[j - 1] >> 32);
+  for (int u = prev + 1; u <= t; ++u) hoff[u] = j;
+  if (j == nh - 1)
+    for (int u = t + 1; u <= ntiles; ++u) hoff[u] = nh;
+}
+
+__global__ void k_fill_int(int n, int* v, int value) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) v[i] = value;
+}
+
+// slots of owned edges (halo slots marked 0xffff, filled by k_slots_halo)
+__global__ void k_slots_owned(int C, int T, const int* i0, const int* i1, const int* i2,
+                              const int* el, const int* er, const int* eoff,
+                              unsigned short* slots) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int t = c / T;
+  const int inc[3] = {i0[c], i1[c], i2[c]};
+  for (int k = 0; k < 3; ++k) {
+    const int e = inc[k] >> 1;
+    slots[4 * (size_t)c + k] = owner_tile(el, er, e, T) == t
+                                   ? (unsigned short)(((e - eoff[t]) << 1) | (inc[k] & 1))
+                                   : (unsigned short)0xffff;
+  }
+  slots[4 * (size_t)c + 3] = 0;
+}
+
+__global__ void k_slots_halo(int nh, const int* halo, const unsigned long long* key,
+                             const int* hoff, const int* eoff, const int* el, const int* er, int T,
+                             const int* i0, const int* i1, const int* i2, unsigned short* slots) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nh) return;
+  const int t = (int)(key[j] >> 32);
+  const int e = halo[j];
+  const int cell = el[e] / T == t ? el[e] : er[e];
+  const int slot = (eoff[t + 1] - eoff[t]) + (j - hoff[t]);
+  const int inc[3] = {i0[cell], i1[cell], i2[cell]};
+  for (int k = 0; k < 3; ++k)
+    if ((inc[k] >> 1) == e) slots[4 * (size_t)cell + k] = (unsigned short)((slot << 1) | (inc[k] & 1));
+}
+
+__global__ void k_slots_check(int C, const unsigned short* slots, int* bad) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  for (int k = 0; k < 3; ++k)
+    if (slots[4 * (size_t)c + k] == 0xffff) atomicExch(bad, 2);
+}
+
+// state permutation: reference order <-> device order
+__global__ void k_state_in(int C, const int* c_orig, const double* h, const double* qx,
+                           const double* qy, double* dh, double* dqx, double* dqy) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  const int o = c_orig[c];
+  dh[c] = h[o];
+  dqx[c] = qx[o];
+  dqy[c] = qy[o];
+}
+
+__global__ void k_state_out(int C, const int* c_new, const double* dh, const double* dqx,
+                            const double* dqy, double* h, double* qx, double* qy) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= C) return;
+  const int c = c_new[o];
+  h[o] = dh[c];
+  qx[o] = dqx[c];
+  qy[o] = dqy[c];
+}
+
+// edge records -> reference left/right Flux3 arrays (compute_fluxes layout)
+__global__ void k_flux_out(Dev d, double* left, double* right) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= d.E) return;
+  const int o = d.e_orig[e];
+  const bool wall_e = d.er[e] < 0;
+  left[3 * (size_t)o] = d.M[e];
+  left[3 * (size_t)o + 1] = d.LX[e];
+  left[3 * (size_t)o + 2] = d.LY[e];
+  right[3 * (size_t)o] = wall_e ? 0.0 : -d.M[e];
+  right[3 * (size_t)o + 1] = wall_e ? 0.0 : d.RX[e];
+  right[3 * (size_t)o + 2] = wall_e ? 0.0 : d.RY[e];
+}
+
+// point physics over arrays (kernel-level parity tests)
+__global__ void k_point(int kind, long long n, Phys P, const double* l, const double* r,
+                        const double* z, const double* nrm, double* out) {
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const Cons a{l[3 * i], l[3 * i + 1], l[3 * i + 2]};
+  if (kind == 0) {
+    const Cons b{r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+    const Flux f = hllc(a, b, nrm[2 * i], nrm[2 * i + 1], P);
+    out[3 * i] = f.m;
+    out[3 * i + 1] = f.fx;
+    out[3 * i + 2] = f.fy;
+  } else if (kind == 1) {
+    const Flux f = wall(a, nrm[2 * i], nrm[2 * i + 1], P);
+    out[3 * i] = f.m;
+    out[3 * i + 1] = f.fx;
+    out[3 * i + 2] = f.fy;
+  } else if (kind == 2) {
+    const Cons b{r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+    double f0, lx, ly, rx, ry;
+    interior_edge(a, z[2 * i], b, z[2 * i + 1], nrm[2 * i], nrm[2 * i + 1], P, f0, lx, ly, rx, ry);
+    out[6 * i] = f0;
+    out[6 * i + 1] = lx;
+    out[6 * i + 2] = ly;
+    out[6 * i + 3] = -f0;
+    out[6 * i + 4] = rx;
+    out[6 * i + 5] = ry;
+  } else if (kind == 3) {
+    const Cons u = friction(a, z[2 * i], z[2 * i + 1], P);
+    out[3 * i] = u.h;
+    out[3 * i + 1] = u.qx;
+    out[3 * i + 2] = u.qy;
+  } else if (kind == 4) {
+    out[i] = swe_pow43(a.h);
+  }
+}
+
+}  // namespace swe_b200

@@ -148,14 +148,15 @@ def digest(*arrays):
     return h.hexdigest()
 
 
+@pytest.mark.parametrize("two_phase", [False, True], ids=["fused", "two_phase"])
 @pytest.mark.parametrize("name", ["water_drop_12x12_200", "still_water_8x8_25", "lake_at_rest_30x12_50",
                                   "dam_break_1d_100x10_t40", "water_drop_50x50_1000",
                                   "three_mounds_100x40_t30"])
-def test_trajectory_vs_reference_golden(golden, coracle, name):
+def test_trajectory_vs_reference_golden(golden, coracle, name, two_phase):
     """Device run loop (one graph launch) against the reference's trajectories."""
     g = golden["trajectories"][name]
     mesh, st = golden_case(g)
-    s = api.DeviceSolver(mesh)
+    s = api.DeviceSolver(mesh, two_phase=two_phase)
     s.set_state(st)
     recs = s.advance(t_end=g["t_end"], max_steps=g["steps"])
     got, t, step = s.get_state()
@@ -167,11 +168,12 @@ def test_trajectory_vs_reference_golden(golden, coracle, name):
     assert s.ledger()[1] == g["clip_events"]
 
 
-def test_config1_circular_dam_break_1000_steps(coracle):
+@pytest.mark.parametrize("two_phase", [False, True], ids=["fused", "two_phase"])
+def test_config1_circular_dam_break_1000_steps(coracle, two_phase):
     """BASELINE configs[0]: ~10k-triangle unstructured circular dam break, 1000 steps."""
     sc = api.make_scenario("circular_dam_break")
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
-    s = api.DeviceSolver(mesh)
+    s = api.DeviceSolver(mesh, two_phase=two_phase)
     s.set_state(sc.state)
     recs = s.advance(t_end=1e30, max_steps=1000)
     got, t, step = s.get_state()
@@ -185,12 +187,13 @@ def test_config1_circular_dam_break_1000_steps(coracle):
     assert abs(m[-1] - m[0]) <= 1e-12 * m[0]
 
 
+@pytest.mark.parametrize("two_phase", [False, True], ids=["fused", "two_phase"])
 @pytest.mark.parametrize("scenario", ["three_mounds_friction", "sloping_wet_dry", "channel"])
-def test_friction_scenarios_scaled(coracle, scenario):
+def test_friction_scenarios_scaled(coracle, scenario, two_phase):
     """Configs 2-4 at reduced resolution: wet/dry fronts + bathymetry + Manning."""
     sc = api.make_scenario(scenario, scale=0.04 if scenario != "three_mounds_friction" else 0.1)
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
-    s = api.DeviceSolver(mesh)
+    s = api.DeviceSolver(mesh, two_phase=two_phase)
     s.set_state(sc.state)
     recs = s.advance(t_end=1e30, max_steps=300)
     got, t, step = s.get_state()
@@ -202,6 +205,34 @@ def test_friction_scenarios_scaled(coracle, scenario):
         assert bit_equal(a, ref[k]), k                    # ... and the one we hold
     assert bit_equal(recs[:, 2], ref["dts"])
     assert s.ledger()[1] == ref["clip_events"]
+
+
+def test_oversized_tile_is_rejected(monkeypatch):
+    monkeypatch.setenv("SWE_TILE_CELLS", "8192")
+    sc = api.make_scenario("sloping_wet_dry", scale=0.03)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    with pytest.raises(api.DeviceError, match="shared memory"):
+        api.DeviceSolver(mesh)
+
+
+@pytest.mark.parametrize("threads", [128, 256])
+@pytest.mark.parametrize("tile_cells", [32, 100, 256, 1024])
+def test_tile_sizes_agree(coracle, monkeypatch, tile_cells, threads):
+    monkeypatch.setenv("SWE_TILE_THREADS", str(threads))
+    """The fused kernel's result does not depend on the tile size (halo edges
+    are evaluated by both tiles from identical inputs)."""
+    monkeypatch.setenv("SWE_TILE_CELLS", str(tile_cells))
+    sc = api.make_scenario("sloping_wet_dry", scale=0.03)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    s = api.DeviceSolver(mesh)
+    assert s.info()["tile_cells"] == tile_cells and s.info()["fused"] == 1
+    s.set_state(sc.state)
+    recs = s.advance(t_end=1e30, max_steps=120)
+    got = s.get_state()[0]
+    ref = coracle.advance(MeshArrays.from_mesh(mesh), sc.state.h, sc.state.qx, sc.state.qy,
+                          nsteps=120)
+    assert bit_equal(got.h, ref["h"]) and bit_equal(got.qx, ref["qx"]) and bit_equal(got.qy, ref["qy"])
+    assert bit_equal(recs[:, 2], ref["dts"])
 
 
 def test_morton_and_identity_order_agree():

@@ -16,18 +16,19 @@ def main():
     ap.add_argument("--scale", type=float, default=1.0)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--identity", action="store_true")
+    ap.add_argument("--two-phase", action="store_true")
     a = ap.parse_args()
     import torch
     from paper_1807_00672_b200 import api
     sc = api.make_scenario(a.config, scale=a.scale)
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
-    s = api.DeviceSolver(mesh, identity_order=a.identity)
+    s = api.DeviceSolver(mesh, identity_order=a.identity, two_phase=a.two_phase)
     s.set_state(sc.state)
     H = 1.7976931348623157e308
     s.advance(t_end=H, max_steps=5)
     st = torch.cuda.ExternalStream(s.stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    out = {"cells": mesh.n_cells, "edges": mesh.n_edges}
+    out = {"cells": mesh.n_cells, "edges": mesh.n_edges, "info": s.info()}
     for rep in range(2):
         _, step0 = s.clock()
         torch.cuda.synchronize()
