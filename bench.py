@@ -273,15 +273,26 @@ def run_b200(args):
     solver.synchronize()
     kt = solver.kernel_times()
     solver.set_profiling(False)
-    face_ms = kt["face"][0] / max(1, kt["face"][1])
-    cell_ms = kt["cell"][0] / max(1, kt["cell"][1])
-    fin_ms = kt["finalize"][0] / max(1, kt["finalize"][1])
+    info = solver.info()
+    avg = lambda k: kt[k][0] / max(1, kt[k][1])  # noqa: E731
+    fin_ms = avg("finalize")
     peak, peak_src = load_peaks()
-    face_bytes = 64 * E + 32 * C
-    cell_bytes = 64 * E + 84 * C
-    dom = ("face", face_ms, face_bytes) if face_ms >= cell_ms else ("cell", cell_ms, cell_bytes)
+    if info["fused"]:
+        # k_tile compulsory traffic: cell state/bed/area/n/r in (56 B) + state
+        # out (24 B); edge el, er, nx, ny, len, kl, kr (34 B); halo index (4 B)
+        tile_ms = avg("tile")
+        kernels = {"tile": tile_ms, "finalize": fin_ms}
+        dom = ("tile", tile_ms, 80 * C + 34 * E + 4 * info["halo_edges"])
+    else:
+        # k_face_c: edge data 34 B + contributions out 48 B per edge, state+bed
+        # gathers 32 B per cell; k_cell_c: 3x3 contributions 72 B + state 24 B
+        # + area/n/r 24 B in, state 24 B out per cell
+        face_ms, cell_ms = avg("face"), avg("cell")
+        kernels = {"face": face_ms, "cell": cell_ms, "finalize": fin_ms}
+        dom = (("face", face_ms, 82 * E + 32 * C) if face_ms >= cell_ms
+               else ("cell", cell_ms, 144 * C))
     achieved = dom[2] / (dom[1] / 1e3) / 1e9
-    step_bytes = 116 * C + 128 * E
+    step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical two-phase B_step
     traffic = None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
@@ -296,15 +307,19 @@ def run_b200(args):
            "config": workload_config(args.config, sc, mesh, world,
                                      {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
                                       "device_bytes": solver.memory_bytes()}),
-           "gpu_launches": 3 * K + 1,
-           "gpu_launches_note": "1 graph launch = gate kernel + K x (face, cell, finalize) "
+           "gpu_launches": (2 if info["fused"] else 3) * K + 1,
+           "gpu_launches_note": "one CUDA-graph launch = k_gate + K x ("
+                                + ("k_tile" if info["fused"] else "k_face_c, k_cell_c")
+                                + ", k_finalize) in a conditional WHILE node "
                                 f"(host-side launch calls: {launches})",
            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                         "peak_source": peak_src,
                         "algorithmic_bytes_per_launch": dom[2],
-                        "kernel_ms": {"face": face_ms, "cell": cell_ms, "finalize": fin_ms},
-                        "step": {"algorithmic_bytes": step_bytes,
+                        "kernel_ms": kernels,
+                        "layout": info,
+                        "step": {"canonical_bytes": "SURVEY.md 8(d) B_step = 116 C + 128 E",
+                                 "algorithmic_bytes": step_bytes,
                                  "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
                                  "frac": step_bytes / (ms / K / 1e3) / 1e9 / peak}},
            "clocks": clk.summary()}

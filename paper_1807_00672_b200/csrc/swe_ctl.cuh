@@ -68,15 +68,17 @@ struct Dev {
   const int *el, *er;  // er < 0: reflective wall
   const double *nx, *ny, *len;
   const int* e_orig;
+  const unsigned char *kl, *kr;  // local index k of the edge in its left / right cell
   // tiles of T consecutive cells (fused path)
-  int T, ntiles, max_slots;
-  const int* eoff;       // [ntiles+1] owned edge range of each tile
-  const int* hoff;       // [ntiles+1] halo list range of each tile
-  const int* halo;       // halo edges (owned by another tile, touching this one)
-  const ushort4* slots;  // per cell: (tile-local slot << 1) | (sign < 0), x3
+  int T, ntiles, max_slots;  // max_slots: most edges (owned + halo) of one tile
+  const int* eoff;  // [ntiles+1] owned edge range of each tile
+  const int* hoff;  // [ntiles+1] halo list range of each tile
+  const int* halo;  // halo edges (owned by another tile, touching this one)
   // state, double-buffered
   double *h[2], *qx[2], *qy[2];
-  // edge records of the two-phase path
+  // per-incidence contributions [3C] of the two-phase step
+  double *TM, *TX, *TY;
+  // edge records [E] of compute_fluxes
   double *M, *LX, *LY, *RX, *RY;
   // control
   Ctl* ctl;

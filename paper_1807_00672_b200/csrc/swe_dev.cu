@@ -70,8 +70,9 @@ struct swe_dev_ctx {
   long long rec_cap = 0;
   double *stage_h = nullptr, *stage_qx = nullptr, *stage_qy = nullptr;
   int grid_face = 0, grid_cell = 0, grid_tile = 0;
-  int tile_threads = 256;
+  int tile_threads = 128;  // measured best with 256-cell tiles (r02)
   size_t tile_smem = 0;
+  int max_slots = 0;  // most edges (owned + halo) one tile evaluates
   long long n_halo = 0;
   // graph
   cudaGraph_t graph = nullptr;
@@ -105,10 +106,10 @@ int launch_update(swe_dev_ctx* x) {  // the step kernel(s) before finalize, 1 or
     ++g_launches;
     return cuda_ok(cudaGetLastError(), "k_tile") ? SWE_OK : SWE_CUDA;
   }
-  k_face<<<x->grid_face, kBlock, 0, x->stream>>>(x->d);
-  k_cell<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
+  k_face_c<<<x->grid_face, kBlock, 0, x->stream>>>(x->d);
+  k_cell_c<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
   g_launches += 2;
-  return cuda_ok(cudaGetLastError(), "k_face/k_cell") ? SWE_OK : SWE_CUDA;
+  return cuda_ok(cudaGetLastError(), "k_face_c/k_cell_c") ? SWE_OK : SWE_CUDA;
 }
 
 int launch_finalize(swe_dev_ctx* x, cudaGraphConditionalHandle h, int use_cond) {
@@ -344,14 +345,14 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   } else {
     k_fill_int<<<blocks_for(d.ntiles + 1), kBlock, 0, s>>>(d.ntiles + 1, hoff, 0);
   }
-  unsigned short* slots = reinterpret_cast<unsigned short*>(const_cast<ushort4*>(d.slots));
-  k_slots_owned<<<blocks_for(C), kBlock, 0, s>>>(C, T, i0, i1, i2, el, er, eoff, slots);
-  if (nh > 0)
-    k_slots_halo<<<blocks_for(nh), kBlock, 0, s>>>(nh, halo, k64b, hoff, eoff, el, er, T, i0, i1,
-                                                   i2, slots);
-  k_slots_check<<<blocks_for(C), kBlock, 0, s>>>(C, slots, flags);
+  unsigned char* kl = const_cast<unsigned char*>(d.kl);
+  unsigned char* kr = const_cast<unsigned char*>(d.kr);
+  ok = ok && cuda_ok(cudaMemsetAsync(kl, 0xff, E, s), "memset") &&
+       cuda_ok(cudaMemsetAsync(kr, 0xff, E, s), "memset");
+  k_local_index<<<blocks_for(C), kBlock, 0, s>>>(C, i0, i1, i2, kl, kr);
+  k_local_check<<<blocks_for(E), kBlock, 0, s>>>(E, er, kl, kr, flags);
   std::vector<int> h_eoff(d.ntiles + 1), h_hoff(d.ntiles + 1);
-  ok = ok && cuda_ok(cudaGetLastError(), "slots") &&
+  ok = ok && cuda_ok(cudaGetLastError(), "local index") &&
        cuda_ok(cudaMemcpyAsync(h_eoff.data(), eoff, sizeof(int) * (d.ntiles + 1),
                                cudaMemcpyDeviceToHost, s), "d2h") &&
        cuda_ok(cudaMemcpyAsync(h_hoff.data(), hoff, sizeof(int) * (d.ntiles + 1),
@@ -362,8 +363,9 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   int max_slots = 1;
   for (int t = 0; t < d.ntiles; ++t)
     max_slots = std::max(max_slots, (h_eoff[t + 1] - h_eoff[t]) + (h_hoff[t + 1] - h_hoff[t]));
-  if (h_flags[0] == 2) return fail_invalid("swe_dev_create: tile slot table incomplete");
-  if (max_slots >= 32767) return fail_invalid("swe_dev_create: tile too large (slots >= 32767)");
+  if (h_flags[0] == 2)
+    return fail_invalid("swe_dev_create: an edge is not referenced by its cells (cell_edges)");
+  x->max_slots = max_slots;
   d.max_slots = max_slots;
   return SWE_OK;
 }
@@ -393,6 +395,10 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
                    swe_dev_ctx** out) {
   if (!m || !params || !out) return fail_invalid("swe_dev_create: null argument");
   if (m->n_cells <= 0 || m->n_edges <= 0) return fail_invalid("swe_dev_create: empty mesh");
+  // PhysParams invariants (SPEC.md kernels module: g > 0, 0 < h_dry, 0 < cfl < 1
+  // is the reference's contract; cfl is not range-checked by it, so neither here)
+  if (!(params->g > 0.0) || !(params->h_dry > 0.0))
+    return fail_invalid("swe_dev_create: PhysParams needs g > 0 and h_dry > 0");
   if (!m->area || !m->inradius || !m->bed || !m->manning || !m->cell_edge || !m->cell_sign ||
       !m->edge_left || !m->edge_right || !m->nx || !m->ny || !m->len)
     return fail_invalid("swe_dev_create: missing mesh array");
@@ -405,6 +411,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   for (long long i = 0; i < 3LL * C; ++i)
     if (m->cell_edge[i] < 0 || m->cell_edge[i] >= E)
       return fail_invalid("swe_dev_create: cell edge out of range");
+  for (int c = 0; c < C; ++c)  // the select-form reconstruction assumes ordered beds
+    if (!std::isfinite(m->bed[c])) return fail_invalid("swe_dev_create: non-finite bathymetry");
 
   auto* x = new swe_dev_ctx();
   x->device = device;
@@ -422,7 +430,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.C = C;
   d.E = E;
   d.P = Phys{params->g, params->h_dry, params->cfl, params->dt_max, params->h_ref};
-  int T = 512;
+  int T = 256;
   if (const char* env = std::getenv("SWE_TILE_CELLS")) T = std::max(32, std::atoi(env));
   if (const char* env = std::getenv("SWE_TILE_THREADS")) x->tile_threads = std::atoi(env) == 128 ? 128 : 256;
   d.T = T;
@@ -446,18 +454,25 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.eoff = x->alloc<int>(d.ntiles + 1);
   d.hoff = x->alloc<int>(d.ntiles + 1);
   d.halo = x->alloc<int>(E);
-  d.slots = x->alloc<ushort4>(C);
+  d.kl = x->alloc<unsigned char>(E);
+  d.kr = x->alloc<unsigned char>(E);
   for (int b = 0; b < 2; ++b) {
     d.h[b] = x->alloc<double>(C);
     d.qx[b] = x->alloc<double>(C);
     d.qy[b] = x->alloc<double>(C);
   }
-  if (!x->fused || true) {  // records: two-phase step and compute_fluxes
-    d.M = x->alloc<double>(E);
-    d.LX = x->alloc<double>(E);
-    d.LY = x->alloc<double>(E);
-    d.RX = x->alloc<double>(E);
-    d.RY = x->alloc<double>(E);
+  // edge records: compute_fluxes (engine.hpp:138-170)
+  d.M = x->alloc<double>(E);
+  d.LX = x->alloc<double>(E);
+  d.LY = x->alloc<double>(E);
+  d.RX = x->alloc<double>(E);
+  d.RY = x->alloc<double>(E);
+  bool two_ok = true;
+  if (!x->fused) {  // per-incidence contributions of the two-phase step
+    d.TM = x->alloc<double>(3 * (size_t)C);
+    d.TX = x->alloc<double>(3 * (size_t)C);
+    d.TY = x->alloc<double>(3 * (size_t)C);
+    two_ok = d.TY != nullptr;
   }
   x->stage_h = x->alloc<double>(C);
   x->stage_qx = x->alloc<double>(C);
@@ -466,7 +481,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   x->sp = x->alloc<StepParams>(1);
   x->rec_cap = 1 << 16;
   x->rec = x->alloc<swe_step_record>(x->rec_cap);
-  if (!x->rec || !x->stage_qy || !d.RY || !d.slots || !d.e_orig) {
+  if (!x->rec || !x->stage_qy || !d.RY || !d.kr || !d.e_orig || !two_ok) {
     g_last_error = "swe_dev_create: cudaMalloc failed";
     return bail(SWE_CUDA);
   }
@@ -482,9 +497,9 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   int occ_face = 0, occ_cell = 0, occ_tile = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_face, k_face, kBlock, 0);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cell, k_cell, kBlock, 0);
-  x->tile_smem = sizeof(double) * (4 * (size_t)d.T + 8 * (size_t)d.max_slots);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_face, k_face_c, kBlock, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cell, k_cell_c, kBlock, 0);
+  x->tile_smem = tile_smem_bytes(d.T, d.max_slots);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if ((long long)x->tile_smem + 1024 > smem_optin) {
@@ -638,9 +653,9 @@ static int plain_step(swe_dev_ctx* x, size_t ev_base) {
     if (prof) CK(cudaEventRecord(x->events[ev_base + 1], x->stream));
     if (prof) CK(cudaEventRecord(x->events[ev_base + 2], x->stream));
   } else {
-    k_face<<<x->grid_face, kBlock, 0, x->stream>>>(x->d);
+    k_face_c<<<x->grid_face, kBlock, 0, x->stream>>>(x->d);
     if (prof) CK(cudaEventRecord(x->events[ev_base + 1], x->stream));
-    k_cell<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
+    k_cell_c<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
     g_launches += 2;
     CK(cudaGetLastError());
     if (prof) CK(cudaEventRecord(x->events[ev_base + 2], x->stream));
@@ -800,7 +815,7 @@ int swe_dev_kernel_times(swe_dev_ctx* x, double* ms, long long* launches, int n)
 
 int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
   if (!x || !out) return fail_invalid("null argument");
-  const long long v[10] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->d.max_slots, x->n_halo,
+  const long long v[10] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
                            x->grid_tile, x->grid_face, x->grid_cell, (long long)x->tile_smem,
                            x->d.E};
   for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];

@@ -132,42 +132,22 @@ __global__ void k_fill_int(int n, int* v, int value) {
   if (i < n) v[i] = value;
 }
 
-// slots of owned edges (halo slots marked 0xffff, filled by k_slots_halo)
-__global__ void k_slots_owned(int C, int T, const int* i0, const int* i1, const int* i2,
-                              const int* el, const int* er, const int* eoff,
-                              unsigned short* slots) {
+// local index k (0..2, the reference's CCW order) of each edge in its left
+// and right cell; every (edge, side) has exactly one writer.  kr of a wall
+// stays 0xff.
+__global__ void k_local_index(int C, const int* i0, const int* i1, const int* i2,
+                              unsigned char* kl, unsigned char* kr) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
-  const int t = c / T;
   const int inc[3] = {i0[c], i1[c], i2[c]};
-  for (int k = 0; k < 3; ++k) {
-    const int e = inc[k] >> 1;
-    slots[4 * (size_t)c + k] = owner_tile(el, er, e, T) == t
-                                   ? (unsigned short)(((e - eoff[t]) << 1) | (inc[k] & 1))
-                                   : (unsigned short)0xffff;
-  }
-  slots[4 * (size_t)c + 3] = 0;
+  for (int k = 0; k < 3; ++k) (inc[k] & 1 ? kr : kl)[inc[k] >> 1] = (unsigned char)k;
 }
 
-__global__ void k_slots_halo(int nh, const int* halo, const unsigned long long* key,
-                             const int* hoff, const int* eoff, const int* el, const int* er, int T,
-                             const int* i0, const int* i1, const int* i2, unsigned short* slots) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= nh) return;
-  const int t = (int)(key[j] >> 32);
-  const int e = halo[j];
-  const int cell = el[e] / T == t ? el[e] : er[e];
-  const int slot = (eoff[t + 1] - eoff[t]) + (j - hoff[t]);
-  const int inc[3] = {i0[cell], i1[cell], i2[cell]};
-  for (int k = 0; k < 3; ++k)
-    if ((inc[k] >> 1) == e) slots[4 * (size_t)cell + k] = (unsigned short)((slot << 1) | (inc[k] & 1));
-}
-
-__global__ void k_slots_check(int C, const unsigned short* slots, int* bad) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  for (int k = 0; k < 3; ++k)
-    if (slots[4 * (size_t)c + k] == 0xffff) atomicExch(bad, 2);
+__global__ void k_local_check(int E, const int* er, const unsigned char* kl,
+                              const unsigned char* kr, int* bad) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  if (kl[e] > 2 || (er[e] >= 0 && kr[e] > 2)) atomicExch(bad, 2);
 }
 
 // state permutation: reference order <-> device order

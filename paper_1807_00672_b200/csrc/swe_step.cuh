@@ -1,27 +1,38 @@
 // swe_step.cuh -- the explicit step kernels.
 //
-//   k_tile   fused one-pass step (default): per tile of T Morton-consecutive
-//            cells, stage the cells' state in shared memory, evaluate the
-//            fluxes of the tile's owned edges and of its halo edges (edges
-//            owned by a neighbouring tile; evaluated by both tiles from the
-//            same inputs, so bit-identical), keep the edge records in shared
-//            memory, then update the tile's cells.
-//   k_face + k_cell   two-phase path (edge records through HBM), also used by
-//            compute_fluxes.
-// Both reproduce engine.hpp:138-170 + :248-290 bit for bit; the cell update
-// also produces the next step's CFL bound and the post-step mass.
+// The reference's cell update (engine.hpp:254-268) sums, for each cell c and
+// local edge k = 0,1,2, the three terms
+//     F.mass * l,   (F.momx - own_c * ox) * l,   (F.momy - own_c * oy) * l
+// with own_c = 0.5 g h_c^2 and (ox, oy) = sign * n.  Every input of a term is
+// known where the edge flux is evaluated (both cells' depths are loaded
+// there), so the edge evaluation emits these per-incidence CONTRIBUTIONS --
+// the very same FP64 values -- into the slot 3c+k of the cell they belong to,
+// and the update reduces three contiguous slots in the reference's order.
+//
+//   k_tile    fused step (default): per tile of T Morton-consecutive cells,
+//             stage the tile's state in shared memory, evaluate the tile's
+//             owned edges and its halo edges (owned by a neighbouring tile,
+//             evaluated by both from identical inputs -> identical bits),
+//             write contributions of in-tile sides to shared memory, update.
+//   k_face_c + k_cell_c   two-phase step: contributions through HBM; the
+//             update is a pure streaming kernel.
+//   k_face    edge records for the compute_fluxes API (engine.hpp:138-170).
+// All reproduce engine.hpp:138-170 + :248-290 bit for bit; the update also
+// produces the next step's CFL bound and the post-step mass.
 #pragma once
 
 #include "swe_ctl.cuh"
 
+// resident-block budgets (registers) measured on B200 at 10M cells (r02):
+// face 5 (48 regs), cell 4 (64), tile 4 x 256-thread equivalents (64 regs)
 #ifndef SWE_FACE_MINB
-#define SWE_FACE_MINB 6
+#define SWE_FACE_MINB 5
 #endif
 #ifndef SWE_CELL_MINB
 #define SWE_CELL_MINB 4
 #endif
 #ifndef SWE_TILE_MINB
-#define SWE_TILE_MINB 3
+#define SWE_TILE_MINB 4
 #endif
 
 namespace swe_b200 {
@@ -32,28 +43,51 @@ struct CellAcc {
   long long ev;
 };
 
-// engine.hpp:254-289 for one cell given its three applied edge fluxes in the
-// reference's local order: (fm, fx, fy) per unit length, edge length l and
-// outward normal (ox, oy) = sign * n.  Writes the new state and accumulates
-// clip ledger, mass and the next step's CFL bound.
-__device__ __forceinline__ void cell_update(const Dev& d, int c, double h, double qx, double qy,
-                                            const double* fm, const double* fx, const double* fy,
-                                            const double* l, const double* ox, const double* oy,
-                                            double dt, double* NH, double* NQX, double* NQY,
-                                            CellAcc& a) {
-  const Phys& P = d.P;
-  const double own = ((0.5 * P.g) * h) * h;  // engine.hpp:254
-  double am = 0.0, ax = 0.0, ay = 0.0;
-#pragma unroll
-  for (int k = 0; k < 3; ++k) {  // engine.hpp:256-264
-    am += fm[k] * l[k];
-    ax += (fx[k] - own * ox[k]) * l[k];
-    ay += (fy[k] - own * oy[k]) * l[k];
+// contributions of one edge to its left / right cell (terms of
+// engine.hpp:261-263); walls contribute to the left cell only
+struct EdgeTerms {
+  double lm, lx, ly, rm, rx, ry;
+};
+
+// evaluate one edge from its two states (engine.hpp:147-166); returns false
+// on a negative depth (engine.hpp:147-153)
+__device__ __forceinline__ bool edge_terms(const Cons& uL, double zl, const Cons& uR, double zr,
+                                           bool is_wall, double nx, double ny, double len,
+                                           const Phys& P, EdgeTerms& t) {
+  const double hg = 0.5 * P.g;
+  const double ownL = (hg * uL.h) * uL.h;
+  if (!is_wall) {
+    if (uL.h < 0.0 || uR.h < 0.0) return false;
+    double f0, lx, ly, rx, ry;
+    interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
+    const double ownR = (hg * uR.h) * uR.h;
+    t.lm = f0 * len;
+    t.lx = (lx - ownL * nx) * len;
+    t.ly = (ly - ownL * ny) * len;
+    t.rm = (-f0) * len;  // right.mass = -f.mass
+    t.rx = (rx - ownR * (-nx)) * len;
+    t.ry = (ry - ownR * (-ny)) * len;
+  } else {
+    if (uL.h < 0.0) return false;
+    const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
+    t.lm = f.m * len;
+    t.lx = (f.fx - ownL * nx) * len;
+    t.ly = (f.fy - ownL * ny) * len;
   }
-  const double area = __ldg(d.area + c);
+  return true;
+}
+
+// engine.hpp:265-289 given the cell's summed fluxes and its area / Manning n /
+// inradius; writes the new state and accumulates the clip ledger, the mass
+// and the next step's CFL bound
+__device__ __forceinline__ void cell_finish_v(const Dev& d, int c, double h, double qx, double qy,
+                                              double am, double ax, double ay, double dt,
+                                              double area, double man, double inr, double* NH,
+                                              double* NQX, double* NQY, CellAcc& a) {
+  const Phys& P = d.P;
   const double scale = dt / area;  // engine.hpp:265-268
   Cons u{h - scale * am, qx - scale * ax, qy - scale * ay};
-  u = friction(u, __ldg(d.man + c), dt, P);  // engine.hpp:269
+  u = friction(u, man, dt, P);  // engine.hpp:269
   if (u.h < -1e-14 * P.h_ref || !isfinite(u.h) || !isfinite(u.qx) || !isfinite(u.qy)) {
     atomicMin(&d.ctl->bad_cell, __ldg(d.c_orig + c));  // engine.hpp:273-279
     NH[c] = u.h;
@@ -77,14 +111,21 @@ __device__ __forceinline__ void cell_update(const Dev& d, int c, double h, doubl
     if (!isfinite(s)) {
       atomicMin(&d.ctl->bad_speed, __ldg(d.c_orig + c));
     } else {
-      a.lo = sel_min(a.lo, __ldg(d.inr + c) / s);
+      a.lo = sel_min(a.lo, inr / s);
       a.hi = sel_max(a.hi, s);
     }
   }
 }
 
+__device__ __forceinline__ void cell_finish(const Dev& d, int c, double h, double qx, double qy,
+                                            double am, double ax, double ay, double dt,
+                                            double* NH, double* NQX, double* NQY, CellAcc& a) {
+  cell_finish_v(d, c, h, qx, qy, am, ax, ay, dt, __ldg(d.area + c), __ldg(d.man + c),
+                __ldg(d.inr + c), NH, NQX, NQY, a);
+}
+
 // ---------------------------------------------------------------------------
-// two-phase path: k_face (engine.hpp:138-170) then k_cell (:248-290)
+// k_face: edge records {f0, left momentum, right momentum} for compute_fluxes
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kBlock, SWE_FACE_MINB) k_face(Dev d) {
   const Ctl* ctl = d.ctl;
@@ -126,7 +167,43 @@ __global__ void __launch_bounds__(kBlock, SWE_FACE_MINB) k_face(Dev d) {
   }
 }
 
-__global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell(Dev d) {
+// ---------------------------------------------------------------------------
+// two-phase step: k_face_c (contributions to HBM) then k_cell_c (streaming)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kBlock, SWE_FACE_MINB) k_face_c(Dev d) {
+  Ctl* ctl = d.ctl;
+  if (!ctl->active) return;
+  const int cur = ctl->cur;
+  const double* __restrict__ H = d.h[cur];
+  const double* __restrict__ QX = d.qx[cur];
+  const double* __restrict__ QY = d.qy[cur];
+  const int stride = gridDim.x * blockDim.x;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d.E; e += stride) {
+    const int cl = __ldg(d.el + e), cr = __ldg(d.er + e);
+    const double nx = __ldg(d.nx + e), ny = __ldg(d.ny + e), len = __ldg(d.len + e);
+    const Cons uL{__ldg(H + cl), __ldg(QX + cl), __ldg(QY + cl)};
+    const bool w = cr < 0;
+    const int crs = w ? cl : cr;
+    const Cons uR{__ldg(H + crs), __ldg(QX + crs), __ldg(QY + crs)};
+    EdgeTerms t;
+    if (!edge_terms(uL, __ldg(d.z + cl), uR, __ldg(d.z + crs), w, nx, ny, len, d.P, t)) {
+      atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
+      continue;
+    }
+    const int sl = 3 * cl + __ldg(d.kl + e);
+    d.TM[sl] = t.lm;
+    d.TX[sl] = t.lx;
+    d.TY[sl] = t.ly;
+    if (!w) {
+      const int sr = 3 * cr + __ldg(d.kr + e);
+      d.TM[sr] = t.rm;
+      d.TX[sr] = t.rx;
+      d.TY[sr] = t.ry;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell_c(Dev d) {
   Ctl* ctl = d.ctl;
   if (!ctl->active) return;
   const int cur = ctl->cur;
@@ -140,31 +217,31 @@ __global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell(Dev d) {
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
   const int stride = gridDim.x * blockDim.x;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C; c += stride) {
-    const int inc[3] = {__ldg(d.inc0 + c), __ldg(d.inc1 + c), __ldg(d.inc2 + c)};
-    double fm[3], fx[3], fy[3], l[3], ox[3], oy[3];
+    double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-      const int e = inc[k] >> 1;
-      const bool neg = inc[k] & 1;
-      const double m = d.M[e];
-      fm[k] = neg ? -m : m;
-      fx[k] = neg ? d.RX[e] : d.LX[e];
-      fy[k] = neg ? d.RY[e] : d.LY[e];
-      l[k] = __ldg(d.len + e);
-      const double enx = __ldg(d.nx + e), eny = __ldg(d.ny + e);
-      ox[k] = neg ? -enx : enx;  // double(sign) * n, engine.hpp:259-260
-      oy[k] = neg ? -eny : eny;
+      am += d.TM[3 * c + k];
+      ax += d.TX[3 * c + k];
+      ay += d.TY[3 * c + k];
     }
-    cell_update(d, c, H[c], QX[c], QY[c], fm, fx, fy, l, ox, oy, dt, NH, NQX, NQY, a);
+    cell_finish(d, c, H[c], QX[c], QY[c], am, ax, ay, dt, NH, NQX, NQY, a);
   }
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
 }
 
 // ---------------------------------------------------------------------------
-// fused tile kernel
-// shared memory: staged tile state [4*T] (h, qx, qy, z) + per slot
-// [8*S] (f0, left mom x/y, right mom x/y, nx, ny, len)
+// fused tile kernel.  Per tile of T Morton-consecutive cells: stage the
+// tile's state and bed in shared memory, evaluate the owned + halo edges into per-incidence contributions in shared
+// memory, update the cells.  Shared memory: state+bed [4T], contributions
+// [9T] -- kept small on purpose: the FP64 dependency chains of the flux need
+// resident warps more than staged data (a variant staging every array needed
+// 65 KB per 256-cell tile and ran 1.3x slower; a TMA bulk L2 prefetch of the
+// next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%, r02).
 // ---------------------------------------------------------------------------
+__host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
+  return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;
+}
+
 template <int NT>
 __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   extern __shared__ double smem[];
@@ -178,26 +255,21 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   double* NH = d.h[cur ^ 1];
   double* NQX = d.qx[cur ^ 1];
   double* NQY = d.qy[cur ^ 1];
-  const int T = d.T, S = d.max_slots;
+  const int T = d.T;
   double* sh = smem;
   double* sq = sh + T;
   double* sr = sq + T;
   double* sz = sr + T;
-  double* rM = sz + T;
-  double* rLX = rM + S;
-  double* rLY = rLX + S;
-  double* rRX = rLY + S;
-  double* rRY = rRX + S;
-  double* rNX = rRY + S;
-  double* rNY = rNX + S;
-  double* rL = rNY + S;
+  double* tm = sz + T;
+  double* tx = tm + 3 * T;
+  double* ty = tx + 3 * T;
   const Phys P = d.P;
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
   for (int t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
     const int c0 = t * T;
     const int nc = min(T, d.C - c0);
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {  // stage the tile
+    for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile
       sh[i] = H[c0 + i];
       sq[i] = QX[c0 + i];
       sr[i] = QY[c0 + i];
@@ -207,80 +279,61 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
     __syncthreads();
 
-    // phase 1: fluxes of owned + halo edges into the slot records
-    for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+    // owned + halo edges -> contributions of the in-tile sides
+    for (int j = threadIdx.x; j < ns; j += NT) {
       const int e = j < no ? e0 + j : __ldg(d.halo + h0 + (j - no));
       const int cl = __ldg(d.el + e), cr = __ldg(d.er + e);
-      const double nx = __ldg(d.nx + e), ny = __ldg(d.ny + e);
-      rNX[j] = nx;
-      rNY[j] = ny;
-      rL[j] = __ldg(d.len + e);
-      const int il = cl - c0;
-      Cons uL;
-      double zl;
-      if ((unsigned)il < (unsigned)nc) {
+      const double nx = __ldg(d.nx + e), ny = __ldg(d.ny + e), len = __ldg(d.len + e);
+      const bool w = cr < 0;
+      const int il = cl - c0, ir = (w ? cl : cr) - c0;
+      const bool inL = (unsigned)il < (unsigned)nc, inR = !w && (unsigned)ir < (unsigned)nc;
+      Cons uL, uR;
+      double zl, zr;
+      if (inL) {
         uL = Cons{sh[il], sq[il], sr[il]};
         zl = sz[il];
       } else {
         uL = Cons{__ldg(H + cl), __ldg(QX + cl), __ldg(QY + cl)};
         zl = __ldg(d.z + cl);
       }
-      if (cr >= 0) {
-        const int ir = cr - c0;
-        Cons uR;
-        double zr;
-        if ((unsigned)ir < (unsigned)nc) {
-          uR = Cons{sh[ir], sq[ir], sr[ir]};
-          zr = sz[ir];
-        } else {
-          uR = Cons{__ldg(H + cr), __ldg(QX + cr), __ldg(QY + cr)};
-          zr = __ldg(d.z + cr);
-        }
-        if (uL.h < 0.0 || uR.h < 0.0) {  // engine.hpp:147-153
-          atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
-          rM[j] = rLX[j] = rLY[j] = rRX[j] = rRY[j] = 0.0;
-          continue;
-        }
-        double f0, lx, ly, rx, ry;
-        interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
-        rM[j] = f0;
-        rLX[j] = lx;
-        rLY[j] = ly;
-        rRX[j] = rx;
-        rRY[j] = ry;
+      if ((unsigned)ir < (unsigned)nc) {
+        uR = Cons{sh[ir], sq[ir], sr[ir]};
+        zr = sz[ir];
       } else {
-        if (uL.h < 0.0) {
-          atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
-          rM[j] = rLX[j] = rLY[j] = 0.0;
-          continue;
-        }
-        const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
-        rM[j] = f.m;
-        rLX[j] = f.fx;
-        rLY[j] = f.fy;
+        const int c = ir + c0;
+        uR = Cons{__ldg(H + c), __ldg(QX + c), __ldg(QY + c)};
+        zr = __ldg(d.z + c);
+      }
+      EdgeTerms et;
+      if (!edge_terms(uL, zl, uR, zr, w, nx, ny, len, P, et)) {
+        atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
+        continue;
+      }
+      if (inL) {
+        const int s = 3 * il + __ldg(d.kl + e);
+        tm[s] = et.lm;
+        tx[s] = et.lx;
+        ty[s] = et.ly;
+      }
+      if (inR) {
+        const int s = 3 * ir + __ldg(d.kr + e);
+        tm[s] = et.rm;
+        tx[s] = et.rx;
+        ty[s] = et.ry;
       }
     }
     __syncthreads();
 
-    // phase 2: cell update from the slot records
-    for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-      const int c = c0 + i;
-      const ushort4 s = d.slots[c];
-      const int sl[3] = {s.x, s.y, s.z};
-      double fm[3], fx[3], fy[3], l[3], ox[3], oy[3];
+    // cell update from the three contribution slots
+    for (int i = threadIdx.x; i < nc; i += NT) {
+      double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
-        const int j = sl[k] >> 1;
-        const bool neg = sl[k] & 1;
-        const double m = rM[j];
-        fm[k] = neg ? -m : m;
-        fx[k] = neg ? rRX[j] : rLX[j];
-        fy[k] = neg ? rRY[j] : rLY[j];
-        l[k] = rL[j];
-        ox[k] = neg ? -rNX[j] : rNX[j];
-        oy[k] = neg ? -rNY[j] : rNY[j];
+        am += tm[3 * i + k];
+        ax += tx[3 * i + k];
+        ay += ty[3 * i + k];
       }
-      cell_update(d, c, sh[i], sq[i], sr[i], fm, fx, fy, l, ox, oy, dt, NH, NQX, NQY, a);
+      cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
     }
     __syncthreads();
   }

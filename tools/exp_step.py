@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--identity", action="store_true")
     ap.add_argument("--two-phase", action="store_true")
+    ap.add_argument("--presteps", type=int, default=0)
     a = ap.parse_args()
     import torch
     from paper_1807_00672_b200 import api
@@ -25,7 +26,7 @@ def main():
     s = api.DeviceSolver(mesh, identity_order=a.identity, two_phase=a.two_phase)
     s.set_state(sc.state)
     H = 1.7976931348623157e308
-    s.advance(t_end=H, max_steps=5)
+    s.advance(t_end=H, max_steps=5 + a.presteps)
     st = torch.cuda.ExternalStream(s.stream)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     out = {"cells": mesh.n_cells, "edges": mesh.n_edges, "info": s.info()}
