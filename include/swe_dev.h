@@ -57,6 +57,10 @@ typedef struct {
   const double* nx;       /* [E] edge_normal.x */
   const double* ny;       /* [E] edge_normal.y */
   const double* len;      /* [E] edge_length */
+  /* multi-device runs: cells [0, n_owned) are owned and updated, the rest
+   * are ghosts (read-only copies of neighbours, refreshed by the halo
+   * exchange); every edge must touch an owned cell.  0 = all owned. */
+  int n_owned;
 } swe_mesh_view;
 
 enum {
@@ -137,6 +141,28 @@ SWE_API int swe_dev_compute_fluxes(swe_dev_ctx* ctx, double* left, double* right
 
 /* total_mass (engine.hpp:128-132) of the current state (fixed-order tree sum). */
 SWE_API int swe_dev_total_mass(swe_dev_ctx* ctx, double* mass);
+
+/* ---- multi-device (domain decomposition, include/swe/partition.hpp) ----
+ * One context per part.  Per step the driver (1) exchanges ghost states --
+ * pack the owned cells peers need into a device buffer, move it (NCCL or a
+ * peer copy), unpack into the ghosts -- (2) reduces the parts' local CFL
+ * bounds (min dts, max max_speed), (3) steps every part with the global
+ * bound.  Cell lists are in the context's reference (local) numbering;
+ * buffers are DEVICE pointers of 3 doubles (h, qx, qy) per cell.  Pack /
+ * unpack complete before returning. */
+SWE_API int swe_dev_set_halo_plan(swe_dev_ctx* ctx, int n_send, const int* send_cells, int n_recv,
+                                  const int* recv_cells);
+SWE_API int swe_dev_pack_halo(swe_dev_ctx* ctx, double* d_buf);
+SWE_API int swe_dev_unpack_halo(swe_dev_ctx* ctx, const double* d_buf);
+/* CFL bound of the owned cells' current state: cfl * min(r / speed) (or
+ * dt_max), max signal speed, owned mass.  Status SWE_NONFINITE_SPEED (with
+ * st->index) if an owned cell has a non-finite speed. */
+SWE_API int swe_dev_local_cfl(swe_dev_ctx* ctx, double* dts, double* max_speed, double* mass,
+                              swe_status* st);
+/* advance_step with the globally reduced bound (engine.hpp:235-237 applied to
+ * dts; max_speed is recorded); rec->mass is the owned mass after the step. */
+SWE_API int swe_dev_step_global(swe_dev_ctx* ctx, double t_end, double dts, double max_speed,
+                                swe_step_record* rec, swe_status* st);
 
 /* Kernel-level timing: when enabled, swe_dev_advance_n_async launches without
  * a graph and brackets every kernel with CUDA events; times accumulate per

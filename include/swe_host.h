@@ -58,6 +58,23 @@ SWE_API void swe_host_mesh_export(void* mesh, int* cell_nodes, double* area, dou
                           int* edge_left, int* edge_right, double* nx, double* ny, double* len);
 SWE_API void swe_host_mesh_free(void* mesh);
 
+/* domain decomposition (include/swe/partition.hpp): part id per cell by
+ * recursive coordinate bisection */
+SWE_API int swe_host_partition(void* mesh, int nparts, int* part_out);
+/* part p's local mesh (owned cells first, then ghosts) and exchange plan */
+SWE_API void* swe_host_local_mesh(void* mesh, const int* part, int p, char* err, int errlen);
+SWE_API void swe_host_local_sizes(void* local, int* n_cells, int* n_owned, int* n_edges,
+                                  int* n_peers, int* n_send, int* n_recv);
+/* arrays in the layout of swe_mesh_view; any output may be NULL */
+SWE_API void swe_host_local_export(void* local, int* cells, int* edges, double* area,
+                                   double* inradius, double* bed, double* manning, double* cx,
+                                   double* cy, int* cell_edge, int* cell_sign, int* edge_left,
+                                   int* edge_right, double* nx, double* ny, double* len);
+/* peers [n_peers]; per peer send/recv counts; flattened cell lists */
+SWE_API void swe_host_local_plan(void* local, int* peers, int* send_counts, int* recv_counts,
+                                 int* send_cells, int* recv_cells);
+SWE_API void swe_host_local_free(void* local);
+
 #ifdef __cplusplus
 }
 #endif

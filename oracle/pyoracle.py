@@ -105,6 +105,36 @@ class COracle:
         L.so_build_mesh.argtypes = [ci, vp, ci, vp] + [vp] * 13
         L.so_batch.restype = None
         L.so_batch.argtypes = [ci, cl, C.POINTER(so_params), vp, vp, vp, vp, vp]
+        L.so_local_cfl.restype = ci
+        L.so_local_cfl.argtypes = [C.POINTER(so_mesh), ci, C.POINTER(so_params), vp, vp, vp,
+                                   C.POINTER(cd), C.POINTER(cd)]
+        L.so_step_owned.restype = ci
+        L.so_step_owned.argtypes = [C.POINTER(so_mesh), ci, C.POINTER(so_params), cd, cd, cd, vp,
+                                    vp, vp, vp, vp, vp, vp, C.POINTER(so_clock),
+                                    C.POINTER(so_step_stats), C.POINTER(ci)]
+
+    # ---- decomposed domain (owned cells first, ghosts after) ----
+    def local_cfl(self, m: "MeshArrays", n_owned, h, qx, qy, params=None):
+        mc, p = m.c(), _params(params)
+        d, s = cd(), cd()
+        bad = self.lib.so_local_cfl(C.byref(mc), n_owned, C.byref(p), P(_c(h)), P(_c(qx)),
+                                    P(_c(qy)), C.byref(d), C.byref(s))
+        return d.value, s.value, bad
+
+    def step_owned(self, m: "MeshArrays", n_owned, state, clk, t_end, dts, max_speed,
+                   params=None):
+        """state: [h, qx, qy] arrays updated in place; clk: so_clock."""
+        mc, p = m.c(), _params(params)
+        out = [np.empty_like(a) for a in state]
+        scratch = np.empty(6 * m.n_edges)
+        st, ei = so_step_stats(), ci()
+        rc = self.lib.so_step_owned(C.byref(mc), n_owned, C.byref(p), t_end, dts, max_speed,
+                                    *[P(a) for a in state], *[P(a) for a in out], P(scratch),
+                                    C.byref(clk), C.byref(st), C.byref(ei))
+        if rc == 0:
+            for a, b in zip(state, out):
+                a[:] = b
+        return rc, st
 
     def point(self, kind, l, r=None, z=None, nrm=None, params=None):
         """so_batch: same kinds and layouts as swe_dev_point_eval."""

@@ -531,3 +531,71 @@ void so_batch(int kind, long n, const so_params* p, const double* l, const doubl
     }
   }
 }
+
+/* ---- decomposed-domain stepping (test infrastructure for the multi-rank
+ * path, include/swe/partition.hpp): cells [0, n_owned) are owned, the rest
+ * ghosts; the CFL bound is reduced across parts by the caller. ---------- */
+
+int so_local_cfl(const so_mesh* m, int n_owned, const so_params* p, const double* h,
+                 const double* qx, const double* qy, double* dts, double* max_speed) {
+  so_mesh part = *m;
+  part.n_cells = n_owned; /* stable_dt_blocks over the owned cells only */
+  return so_stable_dt_blocks(&part, p, h, qx, qy, dts, max_speed);
+}
+
+/* engine.hpp:236-307 with the given bound; ghosts are left untouched */
+int so_step_owned(const so_mesh* m, int n_owned, const so_params* p, double t_end, double dts,
+                  double max_speed, const double* h, const double* qx, const double* qy,
+                  double* nh, double* nqx, double* nqy, double* scratch, so_clock* clk,
+                  so_step_stats* st, int* err_index) {
+  const int last = clk->t + dts >= t_end;
+  const double dt = last ? t_end - clk->t : dts;
+  double* left = scratch;
+  double* right = scratch + 3 * (size_t)m->n_edges;
+  int bad = so_compute_fluxes(m, p, h, qx, qy, left, right);
+  if (bad >= 0) {
+    *err_index = bad;
+    return SO_NEGATIVE_DEPTH;
+  }
+  for (int c = n_owned; c < m->n_cells; ++c) { /* ghosts carry over */
+    nh[c] = h[c];
+    nqx[c] = qx[c];
+    nqy[c] = qy[c];
+  }
+  for (int c = 0; c < n_owned; ++c) {
+    const double own_pressure = 0.5 * p->g * h[c] * h[c];
+    double am = 0.0, ax = 0.0, ay = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      const int e = m->cell_edge[3 * (size_t)c + k];
+      const int sg = m->cell_sign[3 * (size_t)c + k];
+      const double* f = sg > 0 ? left + 3 * (size_t)e : right + 3 * (size_t)e;
+      const double l = m->len[e];
+      am += f[0] * l;
+      ax += (f[1] - own_pressure * (sg * m->nx[e])) * l;
+      ay += (f[2] - own_pressure * (sg * m->ny[e])) * l;
+    }
+    const double scale = dt / m->area[c];
+    so_state u = {h[c] - scale * am, qx[c] - scale * ax, qy[c] - scale * ay};
+    u = so_apply_friction(u, m->manning[c], dt, p);
+    if (u.h < -1e-14 * p->h_ref || !isfinite(u.h) || !isfinite(u.qx) || !isfinite(u.qy)) {
+      *err_index = c;
+      return SO_BLOWUP;
+    }
+    double clipped = 0.0;
+    so_clamp_dry(u, p, &clipped, &u);
+    if (clipped > 0.0) {
+      clk->clipped_volume += clipped * m->area[c];
+      ++clk->clip_events;
+    }
+    nh[c] = u.h;
+    nqx[c] = u.qx;
+    nqy[c] = u.qy;
+  }
+  clk->t = last ? t_end : clk->t + dt;
+  clk->step += 1;
+  st->step = clk->step;
+  st->t = clk->t;
+  st->dt = dt;
+  st->max_speed = max_speed;
+  return SO_OK;
+}

@@ -31,7 +31,8 @@ class swe_mesh_view(C.Structure):
                 ("manning", P_double), ("cx", P_double), ("cy", P_double),
                 ("cell_edge", P_int), ("cell_sign", P_int),
                 ("edge_left", P_int), ("edge_right", P_int),
-                ("nx", P_double), ("ny", P_double), ("len", P_double)]
+                ("nx", P_double), ("ny", P_double), ("len", P_double),
+                ("n_owned", c_int)]
 
 
 class swe_status(C.Structure):
@@ -70,6 +71,13 @@ _SIGS = {
     "swe_dev_set_profiling": (c_int, [c_void_p, c_int]),
     "swe_dev_kernel_times": (c_int, [c_void_p, P_double, P_ll, c_int]),
     "swe_dev_info": (c_int, [c_void_p, P_ll, c_int]),
+    "swe_dev_set_halo_plan": (c_int, [c_void_p, c_int, c_void_p, c_int, c_void_p]),
+    "swe_dev_pack_halo": (c_int, [c_void_p, c_void_p]),
+    "swe_dev_unpack_halo": (c_int, [c_void_p, c_void_p]),
+    "swe_dev_local_cfl": (c_int, [c_void_p, P_double, P_double, P_double,
+                                  C.POINTER(swe_status)]),
+    "swe_dev_step_global": (c_int, [c_void_p, c_double, c_double, c_double,
+                                    C.POINTER(swe_step_record), C.POINTER(swe_status)]),
     "swe_dev_stream": (c_void_p, [c_void_p]),
     "swe_dev_memory_bytes": (c_ll, [c_void_p]),
     "swe_dev_launch_count": (c_ll, []),
@@ -97,6 +105,12 @@ _SIGS = {
     "swe_host_mesh_sizes": (None, [c_void_p, P_int, P_int, P_int]),
     "swe_host_mesh_export": (None, [c_void_p] + [c_void_p] * 13),
     "swe_host_mesh_free": (None, [c_void_p]),
+    "swe_host_partition": (c_int, [c_void_p, c_int, c_void_p]),
+    "swe_host_local_mesh": (c_void_p, [c_void_p, c_void_p, c_int, c_char_p, c_int]),
+    "swe_host_local_sizes": (None, [c_void_p] + [P_int] * 6),
+    "swe_host_local_export": (None, [c_void_p] + [c_void_p] * 15),
+    "swe_host_local_plan": (None, [c_void_p] + [c_void_p] * 5),
+    "swe_host_local_free": (None, [c_void_p]),
     # the C++ drop-in engine behind reference-shaped entry points
     "swe_api_compute_fluxes": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p, c_int, c_char_p, c_int]),

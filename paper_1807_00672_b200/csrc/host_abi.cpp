@@ -6,6 +6,7 @@
 
 #include "swe/cases.hpp"
 #include "swe/engine.hpp"
+#include "swe/partition.hpp"
 #include "swe/mesh.hpp"
 #include "swe_host.h"
 
@@ -374,3 +375,82 @@ EXPORT int swe_api_run(void* mp, const double* params, double* h, double* qx, do
   *step = sim.step;
   return rc;
 }
+
+// ---- domain decomposition (include/swe/partition.hpp) ----------------------
+
+EXPORT int swe_host_partition(void* mp, int nparts, int* part_out) {
+  try {
+    const std::vector<int> p = swe::rcb_partition(*static_cast<swe::Mesh*>(mp), nparts);
+    std::memcpy(part_out, p.data(), sizeof(int) * p.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return kind_of(e);
+  }
+}
+
+EXPORT void* swe_host_local_mesh(void* mp, const int* part, int p, char* err, int errlen) {
+  try {
+    const auto& m = *static_cast<swe::Mesh*>(mp);
+    const std::vector<int> pv(part, part + m.n_cells());
+    return new swe::LocalMesh(swe::build_local_mesh(m, pv, p));
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return nullptr;
+  }
+}
+
+EXPORT void swe_host_local_sizes(void* lp, int* n_cells, int* n_owned, int* n_edges, int* n_peers,
+                                 int* n_send, int* n_recv) {
+  const auto& L = *static_cast<swe::LocalMesh*>(lp);
+  *n_cells = static_cast<int>(L.cells.size());
+  *n_owned = L.n_owned;
+  *n_edges = static_cast<int>(L.edges.size());
+  *n_peers = static_cast<int>(L.peers.size());
+  int s = 0, r = 0;
+  for (size_t i = 0; i < L.peers.size(); ++i) {
+    s += static_cast<int>(L.send[i].size());
+    r += static_cast<int>(L.recv[i].size());
+  }
+  *n_send = s;
+  *n_recv = r;
+}
+
+EXPORT void swe_host_local_export(void* lp, int* cells, int* edges, double* area, double* inradius,
+                                  double* bed, double* manning, double* cx, double* cy,
+                                  int* cell_edge, int* cell_sign, int* edge_left, int* edge_right,
+                                  double* nx, double* ny, double* len) {
+  const auto& L = *static_cast<swe::LocalMesh*>(lp);
+  auto cp = [](auto* dst, const auto& v) {
+    if (dst) std::memcpy(dst, v.data(), sizeof(v[0]) * v.size());
+  };
+  cp(cells, L.cells);
+  cp(edges, L.edges);
+  cp(area, L.area);
+  cp(inradius, L.inradius);
+  cp(bed, L.bed);
+  cp(manning, L.manning);
+  cp(cx, L.cx);
+  cp(cy, L.cy);
+  cp(cell_edge, L.cell_edge);
+  cp(cell_sign, L.cell_sign);
+  cp(edge_left, L.edge_left);
+  cp(edge_right, L.edge_right);
+  cp(nx, L.nx);
+  cp(ny, L.ny);
+  cp(len, L.len);
+}
+
+EXPORT void swe_host_local_plan(void* lp, int* peers, int* send_counts, int* recv_counts,
+                                int* send_cells, int* recv_cells) {
+  const auto& L = *static_cast<swe::LocalMesh*>(lp);
+  int s = 0, r = 0;
+  for (size_t i = 0; i < L.peers.size(); ++i) {
+    peers[i] = L.peers[i];
+    send_counts[i] = static_cast<int>(L.send[i].size());
+    recv_counts[i] = static_cast<int>(L.recv[i].size());
+    for (int c : L.send[i]) send_cells[s++] = c;
+    for (int c : L.recv[i]) recv_cells[r++] = c;
+  }
+}
+
+EXPORT void swe_host_local_free(void* lp) { delete static_cast<swe::LocalMesh*>(lp); }

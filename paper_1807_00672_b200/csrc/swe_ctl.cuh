@@ -59,6 +59,10 @@ struct Part {  // one block's partial results
 
 struct Dev {
   int C, E;
+  int C_own;  // cells [0, C_own) are owned (updated); [C_own, C) are ghosts of a multi-device run
+  // halo exchange plan (device ids): owned cells to pack, ghost cells to unpack
+  int n_send, n_recv;
+  const int *send_cells, *recv_cells;
   // cells (device order)
   const double *area, *inr, *z, *man;
   const int *inc0, *inc1, *inc2;  // (device edge << 1) | (sign < 0), reference local order
@@ -140,7 +144,7 @@ __global__ void __launch_bounds__(kBlock) k_cfl(Dev d) {
   const double* __restrict__ QY = d.qy[cur];
   double lo = INFINITY, hi = 0.0, mass = 0.0;
   const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C; c += stride) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C_own; c += stride) {
     const Cons u{H[c], QX[c], QY[c]};
     mass += u.h * __ldg(d.area + c);
     if (u.h < d.P.h_dry) continue;

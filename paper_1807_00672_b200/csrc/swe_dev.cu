@@ -71,6 +71,8 @@ struct swe_dev_ctx {
   double *stage_h = nullptr, *stage_qx = nullptr, *stage_qy = nullptr;
   int grid_face = 0, grid_cell = 0, grid_tile = 0;
   int tile_threads = 128;  // measured best with 256-cell tiles (r02)
+  int* halo_send = nullptr;  // device ids of the halo plan
+  int* halo_recv = nullptr;
   size_t tile_smem = 0;
   int max_slots = 0;  // most edges (owned + halo) one tile evaluates
   long long n_halo = 0;
@@ -269,29 +271,30 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   int* c_new = const_cast<int*>(d.c_new);
   int* e_orig = const_cast<int*>(d.e_orig);
 
-  // 1. cells: Morton order of centroids (stable: ties keep reference order)
+  // 1. cells: Morton order of the owned cells' centroids (stable: ties keep
+  //    reference order); ghost cells keep their place after the owned ones
+  const int Co = d.C_own;
   const bool morton = !(x->flags & SWE_FLAG_IDENTITY_ORDER) && m->cx && m->cy;
+  if (ok) k_iota<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig);
   if (ok && morton) {
     double x0 = m->cx[0], x1 = x0, y0 = m->cy[0], y1 = y0;
-    for (int c = 1; c < C; ++c) {
+    for (int c = 1; c < Co; ++c) {
       x0 = std::min(x0, m->cx[c]);
       x1 = std::max(x1, m->cx[c]);
       y0 = std::min(y0, m->cy[c]);
       y1 = std::max(y1, m->cy[c]);
     }
     const double span = std::max(x1 - x0, y1 - y0);
-    double* dcx = (double*)tmp.get(sizeof(double) * C);
-    double* dcy = (double*)tmp.get(sizeof(double) * C);
+    double* dcx = (double*)tmp.get(sizeof(double) * Co);
+    double* dcy = (double*)tmp.get(sizeof(double) * Co);
     unsigned* kin = (unsigned*)k64a;
     unsigned* kout = (unsigned*)k64b;
-    ok = dcx && dcy && up(dcx, m->cx, sizeof(double) * C) && up(dcy, m->cy, sizeof(double) * C);
+    ok = dcx && dcy && up(dcx, m->cx, sizeof(double) * Co) && up(dcy, m->cy, sizeof(double) * Co);
     if (ok) {
-      k_morton<<<blocks_for(C), kBlock, 0, s>>>(C, dcx, dcy, x0, y0, span > 0 ? 65535.0 / span : 0.0,
-                                                 kin, idx);
-      ok = radix_sort(tmp, kin, kout, idx, c_orig, C, 32, s);
+      k_morton<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
+                                                  span > 0 ? 65535.0 / span : 0.0, kin, idx);
+      ok = radix_sort(tmp, kin, kout, idx, c_orig, Co, 32, s);
     }
-  } else if (ok) {
-    k_iota<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig);
   }
   if (ok) k_invert<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig, c_new);
 
@@ -328,7 +331,7 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   int* hcount = flags + 1;
   if (ok) {
     k_tile_bounds<<<blocks_for(E), kBlock, 0, s>>>(E, el, er, T, d.ntiles, eoff);
-    k_halo_keys<<<blocks_for(E), kBlock, 0, s>>>(E, el, er, T, k64a, hcount);
+    k_halo_keys<<<blocks_for(E), kBlock, 0, s>>>(E, el, er, T, Co, k64a, hcount);
     ok = cuda_ok(cudaGetLastError(), "tile tables");
   }
   int h_flags[2] = {0, 0};
@@ -413,6 +416,12 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
       return fail_invalid("swe_dev_create: cell edge out of range");
   for (int c = 0; c < C; ++c)  // the select-form reconstruction assumes ordered beds
     if (!std::isfinite(m->bed[c])) return fail_invalid("swe_dev_create: non-finite bathymetry");
+  if (m->n_owned < 0 || m->n_owned > C) return fail_invalid("swe_dev_create: n_owned out of range");
+  if (m->n_owned > 0) {  // every edge of a partial mesh must touch an owned cell
+    for (int e = 0; e < E; ++e)
+      if (m->edge_left[e] >= m->n_owned && (m->edge_right[e] < 0 || m->edge_right[e] >= m->n_owned))
+        return fail_invalid("swe_dev_create: an edge touches no owned cell");
+  }
 
   auto* x = new swe_dev_ctx();
   x->device = device;
@@ -429,12 +438,13 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   Dev& d = x->d;
   d.C = C;
   d.E = E;
+  d.C_own = (m->n_owned > 0 && m->n_owned <= C) ? m->n_owned : C;
   d.P = Phys{params->g, params->h_dry, params->cfl, params->dt_max, params->h_ref};
   int T = 256;
   if (const char* env = std::getenv("SWE_TILE_CELLS")) T = std::max(32, std::atoi(env));
   if (const char* env = std::getenv("SWE_TILE_THREADS")) x->tile_threads = std::atoi(env) == 128 ? 128 : 256;
   d.T = T;
-  d.ntiles = (C + T - 1) / T;
+  d.ntiles = (d.C_own + T - 1) / T;
 
   d.area = x->alloc<double>(C);
   d.inr = x->alloc<double>(C);
@@ -550,6 +560,8 @@ int swe_dev_destroy(swe_dev_ctx* x) {
   if (x->graph) cudaGraphDestroy(x->graph);
   for (cudaEvent_t e : x->events) cudaEventDestroy(e);
   for (void* p : x->allocs) cudaFree(p);
+  cudaFree(x->halo_send);
+  cudaFree(x->halo_recv);
   if (x->h_ctl) cudaFreeHost(x->h_ctl);
   if (x->h_sp) cudaFreeHost(x->h_sp);
   if (x->stream) cudaStreamDestroy(x->stream);
@@ -739,6 +751,104 @@ int swe_dev_advance_n_async(swe_dev_ctx* x, long long n, double t_end) {
     }
   }
   return SWE_OK;
+}
+
+int swe_dev_set_halo_plan(swe_dev_ctx* x, int n_send, const int* send_cells, int n_recv,
+                          const int* recv_cells) {
+  if (!x || n_send < 0 || n_recv < 0 || (n_send && !send_cells) || (n_recv && !recv_cells))
+    return fail_invalid("swe_dev_set_halo_plan: bad argument");
+  for (int i = 0; i < n_send; ++i)
+    if (send_cells[i] < 0 || send_cells[i] >= x->d.C_own)
+      return fail_invalid("swe_dev_set_halo_plan: send cell is not owned");
+  for (int i = 0; i < n_recv; ++i)
+    if (recv_cells[i] < x->d.C_own || recv_cells[i] >= x->d.C)
+      return fail_invalid("swe_dev_set_halo_plan: recv cell is not a ghost");
+  cudaFree(x->halo_send);
+  cudaFree(x->halo_recv);
+  x->halo_send = x->halo_recv = nullptr;
+  CK(cudaMalloc(&x->halo_send, sizeof(int) * (size_t)std::max(1, n_send)));
+  CK(cudaMalloc(&x->halo_recv, sizeof(int) * (size_t)std::max(1, n_recv)));
+  if (n_send)
+    CK(cudaMemcpyAsync(x->halo_send, send_cells, sizeof(int) * n_send, cudaMemcpyHostToDevice,
+                       x->stream));
+  if (n_recv)
+    CK(cudaMemcpyAsync(x->halo_recv, recv_cells, sizeof(int) * n_recv, cudaMemcpyHostToDevice,
+                       x->stream));
+  // reference-local ids -> device ids
+  if (n_send) k_map_cells<<<blocks_for(n_send), kBlock, 0, x->stream>>>(n_send, x->d.c_new, x->halo_send);
+  if (n_recv) k_map_cells<<<blocks_for(n_recv), kBlock, 0, x->stream>>>(n_recv, x->d.c_new, x->halo_recv);
+  CK(cudaGetLastError());
+  x->d.n_send = n_send;
+  x->d.n_recv = n_recv;
+  x->d.send_cells = x->halo_send;
+  x->d.recv_cells = x->halo_recv;
+  CK(cudaStreamSynchronize(x->stream));
+  return SWE_OK;
+}
+
+int swe_dev_pack_halo(swe_dev_ctx* x, double* buf) {
+  if (!x || (x->d.n_send && !buf)) return fail_invalid("swe_dev_pack_halo: bad argument");
+  if (x->d.n_send) {
+    k_halo_pack<<<blocks_for(x->d.n_send), kBlock, 0, x->stream>>>(x->d, buf);
+    ++g_launches;
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(x->stream));
+  return SWE_OK;
+}
+
+int swe_dev_unpack_halo(swe_dev_ctx* x, const double* buf) {
+  if (!x || (x->d.n_recv && !buf)) return fail_invalid("swe_dev_unpack_halo: bad argument");
+  if (x->d.n_recv) {
+    k_halo_unpack<<<blocks_for(x->d.n_recv), kBlock, 0, x->stream>>>(x->d, buf);
+    ++g_launches;
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(x->stream));
+  return SWE_OK;
+}
+
+int swe_dev_local_cfl(swe_dev_ctx* x, double* dts, double* max_speed, double* mass,
+                      swe_status* st) {
+  if (!x) return fail_invalid("null context");
+  if (int rc = ensure_cfl(x)) return rc;
+  if (int rc = sync_ctl(x)) return rc;
+  const Ctl& c = *x->h_ctl;
+  if (dts) *dts = c.dts;
+  if (max_speed) *max_speed = c.max_speed;
+  if (mass) *mass = c.mass;
+  if (c.cfl_bad != kNone) {
+    if (st) {
+      st->code = SWE_NONFINITE_SPEED;
+      st->index = c.cfl_bad;
+    }
+    return SWE_NONFINITE_SPEED;
+  }
+  if (st) st->code = SWE_OK;
+  return SWE_OK;
+}
+
+int swe_dev_step_global(swe_dev_ctx* x, double t_end, double dts, double max_speed,
+                        swe_step_record* rec, swe_status* st) {
+  if (!x) return fail_invalid("null context");
+  if (int rc = ensure_cfl(x)) return rc;
+  if (int rc = sync_ctl(x)) return rc;
+  x->h_ctl->dts = dts;
+  x->h_ctl->max_speed = max_speed;
+  x->h_ctl->cfl_valid = 1;
+  x->h_ctl->cfl_bad = kNone;  // the driver checked every part's bound
+  CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, x->stream));
+  if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, 1, 0, 1)) return rc;
+  if (int rc = launch_gate(x)) return rc;
+  const bool prof = x->profiling;
+  x->profiling = false;
+  const int rc = plain_step(x, 0);
+  x->profiling = prof;
+  if (rc) return rc;
+  const int code = read_status(x, st);
+  if (code == SWE_OK && rec)
+    CK(cudaMemcpy(rec, x->rec, sizeof(swe_step_record), cudaMemcpyDeviceToHost));
+  return code;
 }
 
 int swe_dev_synchronize(swe_dev_ctx* x, swe_status* st) {

@@ -102,13 +102,15 @@ __global__ void k_tile_bounds(int E, const int* el, const int* er, int T, int nt
     for (int t = ow + 1; t <= ntiles; ++t) eoff[t] = E;
 }
 
-// interior edges crossing a tile boundary -> (tile of the upper cell, edge)
-__global__ void k_halo_keys(int E, const int* el, const int* er, int T, unsigned long long* key,
-                            int* count) {
+// interior edges between owned cells of different tiles -> (tile of the
+// upper cell, edge).  Edges to a ghost cell (device id >= C_own) belong to
+// the owned cell's tile alone.
+__global__ void k_halo_keys(int E, const int* el, const int* er, int T, int C_own,
+                            unsigned long long* key, int* count) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   const int r = er[e];
-  if (r < 0) return;
+  if (r < 0 || r >= C_own || el[e] >= C_own) return;
   const int a = el[e] / T, b = r / T;
   if (a == b) return;
   const int slot = atomicAdd(count, 1);
@@ -148,6 +150,31 @@ __global__ void k_local_check(int E, const int* er, const unsigned char* kl,
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= E) return;
   if (kl[e] > 2 || (er[e] >= 0 && kr[e] > 2)) atomicExch(bad, 2);
+}
+
+// multi-device halo exchange: owned cells' current state -> buffer (h, qx, qy
+// interleaved), buffer -> ghost cells' current state
+__global__ void k_halo_pack(Dev d, double* buf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.n_send) return;
+  const int cur = d.ctl->cur, c = d.send_cells[i];
+  buf[3 * (size_t)i] = d.h[cur][c];
+  buf[3 * (size_t)i + 1] = d.qx[cur][c];
+  buf[3 * (size_t)i + 2] = d.qy[cur][c];
+}
+
+__global__ void k_halo_unpack(Dev d, const double* buf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= d.n_recv) return;
+  const int cur = d.ctl->cur, c = d.recv_cells[i];
+  d.h[cur][c] = buf[3 * (size_t)i];
+  d.qx[cur][c] = buf[3 * (size_t)i + 1];
+  d.qy[cur][c] = buf[3 * (size_t)i + 2];
+}
+
+__global__ void k_map_cells(int n, const int* c_new, int* cells) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) cells[i] = c_new[cells[i]];
 }
 
 // state permutation: reference order <-> device order

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell_c(Dev d) {
   double* NQY = d.qy[cur ^ 1];
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
   const int stride = gridDim.x * blockDim.x;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C; c += stride) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < d.C_own; c += stride) {
     double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
 
   for (int t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
     const int c0 = t * T;
-    const int nc = min(T, d.C - c0);
+    const int nc = min(T, d.C_own - c0);
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile
       sh[i] = H[c0 + i];
       sq[i] = QX[c0 + i];

@@ -1,0 +1,170 @@
+"""Domain decomposition on CPU: the partitioner and local
+meshes of the product (include/swe/partition.hpp) driven by the C oracle as
+per-part compute, in one process and across 2 gloo ranks.  A P-part run must
+be bit-identical to the single-domain run."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+from conftest import bit_equal
+from oracle.pyoracle import COracle, MeshArrays, so_clock
+from paper_1807_00672_b200 import api, dist
+
+
+def scenario(name="sloping_wet_dry", scale=0.02):
+    sc = api.make_scenario(name, scale=scale)
+    return sc, api.build_mesh(sc.raw, sc.bed, sc.manning)
+
+
+def local_arrays(lm):
+    a = lm.arrays
+    return MeshArrays(a["area"], a["inradius"], a["bed"], a["manning"], a["cell_edge"],
+                      a["cell_sign"], a["edge_left"], a["edge_right"], a["nx"], a["ny"], a["len"])
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 7, 8])
+def test_partition_and_plans(P):
+    sc, m = scenario()
+    part = dist.partition(m, P)
+    counts = np.bincount(part, minlength=P)
+    assert counts.min() >= counts.max() - 1  # RCB splits by count
+    lms = [dist.local_mesh(m, part, p) for p in range(P)]
+    owned = np.concatenate([lm.cells[:lm.n_owned] for lm in lms])
+    assert np.array_equal(np.sort(owned), np.arange(m.n_cells))
+    edge_count = np.zeros(m.n_edges, int)
+    for lm in lms:
+        edge_count[lm.edges] += 1
+        # owned cells keep their three incidences in reference order
+        ce = lm.arrays["cell_edge"].reshape(-1, 3)[:lm.n_owned]
+        cs = lm.arrays["cell_sign"].reshape(-1, 3)[:lm.n_owned]
+        g = lm.cells[:lm.n_owned]
+        assert np.array_equal(lm.edges[ce], m.cell_edge[g]) and np.array_equal(cs, m.cell_sign[g])
+        for i, q in enumerate(lm.peers):
+            other = lms[q]
+            j = other.peers.index(lm.part)
+            assert np.array_equal(lm.cells[lm.send[i]], other.cells[other.recv[j]])
+    cut = (m.edge_right >= 0) & (part[m.edge_left] != part[np.maximum(m.edge_right, 0)])
+    assert np.all(edge_count[cut] == 2) and np.all(edge_count[~cut] == 1)
+
+
+def oracle_parts_run(m, st, lms, nsteps, exchange_fn, min_fn=lambda x: x, max_fn=lambda x: x):
+    """Step the parts with the oracle; exchange_fn(states) refreshes ghosts;
+    min_fn / max_fn reduce a local value across ranks (identity in-process)."""
+    co = COracle()
+    arrs = [local_arrays(lm) for lm in lms]
+    states = [[np.ascontiguousarray(a[lm.cells]) for a in (st.h, st.qx, st.qy)] for lm in lms]
+    clks = [so_clock(0.0, 0, 0.0, 0) for _ in lms]
+    dts_seq = []
+    for _ in range(nsteps):
+        exchange_fn(states)
+        loc = [co.local_cfl(a, lm.n_owned, *s) for a, lm, s in zip(arrs, lms, states)]
+        assert all(x[2] == -1 for x in loc)
+        dts = min_fn(min(x[0] for x in loc))
+        ms = max_fn(max(x[1] for x in loc))
+        for a, lm, s, clk in zip(arrs, lms, states, clks):
+            rc, stt = co.step_owned(a, lm.n_owned, s, clk, 1e30, dts, ms)
+            assert rc == 0
+        dts_seq.append(stt.dt)
+    return states, dts_seq
+
+
+@pytest.mark.parametrize("P", [2, 3, 5])
+def test_decomposed_oracle_matches_single_domain(P):
+    sc, m = scenario()
+    part = dist.partition(m, P)
+    lms = [dist.local_mesh(m, part, p) for p in range(P)]
+    by_part = {lm.part: lm for lm in lms}
+
+    def exchange(states):
+        for lm, s in zip(lms, states):
+            for i, q in enumerate(lm.peers):
+                other = by_part[q]
+                j = other.peers.index(lm.part)
+                src = states[q]
+                for k in range(3):
+                    s[k][lm.recv[i]] = src[k][other.send[j]]
+
+    states, dts = oracle_parts_run(m, sc.state, lms, 60, exchange)
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=60)
+    assert bit_equal(np.array(dts), ref["dts"])
+    for lm, s in zip(lms, states):
+        own = lm.cells[:lm.n_owned]
+        for k, key in enumerate(("h", "qx", "qy")):
+            assert bit_equal(s[k][:lm.n_owned], ref[key][own]), key
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gloo_worker(rank, world, port, q):
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, m = scenario()
+        part = dist.partition(m, world)
+        lm = dist.local_mesh(m, part, rank)
+
+        def exchange(states):
+            s = states[0]
+            ops, bufs = [], []
+            for i, peer in enumerate(lm.peers):
+                send = torch.from_numpy(np.stack([a[lm.send[i]] for a in s], 1).ravel().copy())
+                recv = torch.empty(3 * len(lm.recv[i]), dtype=torch.float64)
+                ops += [tdist.P2POp(tdist.isend, send, peer), tdist.P2POp(tdist.irecv, recv, peer)]
+                bufs.append((i, recv))
+            for r in tdist.batch_isend_irecv(ops):
+                r.wait()
+            for i, recv in bufs:
+                v = recv.numpy().reshape(-1, 3)
+                for k in range(3):
+                    s[k][lm.recv[i]] = v[:, k]
+
+        def red(x, op):
+            t = torch.tensor([x], dtype=torch.float64)
+            tdist.all_reduce(t, op=op)
+            return float(t.item())
+
+        states, dts = oracle_parts_run(m, sc.state, [lm], 40, exchange,
+                                       lambda x: red(x, tdist.ReduceOp.MIN),
+                                       lambda x: red(x, tdist.ReduceOp.MAX))
+        owned = np.zeros((3, m.n_cells))
+        mask = np.zeros(m.n_cells)
+        for k in range(3):
+            owned[k][lm.cells[:lm.n_owned]] = states[0][k][:lm.n_owned]
+        mask[lm.cells[:lm.n_owned]] = 1
+        t_owned, t_mask = torch.from_numpy(owned), torch.from_numpy(mask)
+        tdist.all_reduce(t_owned)  # disjoint ownership: the sum assembles the field
+        tdist.all_reduce(t_mask)
+        if rank == 0:
+            q.put((t_owned.numpy().copy(), t_mask.numpy().copy(), np.array(dts)))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_two_ranks_match_single_domain():
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    field, mask, dts = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sc, m = scenario()
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=40)
+    assert np.all(mask == 1)
+    assert bit_equal(dts, ref["dts"])
+    for k, key in enumerate(("h", "qx", "qy")):
+        assert bit_equal(field[k], ref[key]), key
