@@ -65,6 +65,8 @@ def parse():
                     help="target CPU work of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                    help="N > 1: strong = the configured mesh split N ways; weak = N x the cells")
     return ap.parse_args()
 
 
@@ -207,12 +209,83 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * phase_s / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(args.config, sc, mesh, 1),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
                             "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
+
+
+def run_b200_dist(args, rank, local, world):
+    """N > 1: the mesh split across ranks by RCB (one part per GPU), ghost
+    layers refreshed by NCCL send/recv, CFL bound by NCCL all_reduce
+    (paper_1807_00672_b200/dist.py).  strong: the configured mesh; weak: the
+    generator resolution scaled by sqrt(N) (N x the cells)."""
+    import torch
+    import torch.distributed as tdist
+    from paper_1807_00672_b200 import api, dist
+
+    scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
+    sc, mesh, setup_s = build_workload(args.config, scale)
+    part = dist.partition(mesh, world)
+    lm = dist.local_mesh(mesh, part, rank)
+    ps = dist.PartSolver(lm, device=local)
+    ex = dist.TorchExchange(ps)
+    ps.set_state(sc.state)
+    W, K = max(3, args.warmup), args.steps
+    dist.run_parts([ps], ex, W)
+    stream = torch.cuda.ExternalStream(dist_stream(ps), device=local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    tdist.barrier()
+    torch.cuda.synchronize()
+    clk = ClockSampler(local).start() if rank == 0 else None
+    w0 = time.time()
+    ev0.record(stream)
+    recs = dist.run_parts([ps], ex, K)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.mark(w0, time.time())
+        clk.stop()
+    ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    ms = float(ms.item())
+    C = mesh.n_cells
+    # e2e: host state in, K steps, owned state back to the host
+    tdist.barrier()
+    t0 = time.perf_counter()
+    ps.set_state(sc.state)
+    dist.run_parts([ps], ex, K)
+    got = api.FieldState.zeros(C)
+    ps.gather_owned(got)
+    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    tdist.all_reduce(e2e_s, op=tdist.ReduceOp.MAX)
+    if rank == 0:
+        out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
+               "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
+               "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": workload_config(args.config, sc, mesh, 1, {
+                   "parallelism": f"{world}-way RCB domain decomposition, one part per GPU, "
+                                  "ghost exchange NCCL send/recv + CFL all_reduce per step "
+                                  "(host-driven)",
+                   "cells_per_gpu_max": int(np.bincount(part).max()),
+                   "halo_cells_rank0": int(lm.n_cells - lm.n_owned), "setup_s": round(setup_s, 2)}),
+               "gpu_launches": None,
+               "gpu_launches_note": "per step and rank: halo pack/unpack, k_gate, k_tile, "
+                                    "k_finalize (+ NCCL kernels)",
+               "clocks": clk.summary() if clk else None,
+               "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
+                       "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": 24 * C / K,
+                       "path": "PartSolver.set_state (host) + K steps + gather_owned (host)"},
+               "step_dt_last": float(recs[-1, 1])}
+        print(json.dumps(out))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def dist_stream(part_solver):
+    return part_solver.lib.swe_dev_stream(part_solver.ctx)
 
 
 def run_b200(args):
@@ -226,6 +299,7 @@ def run_b200(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_b200_dist(args, rank, local, world)
 
     sc, mesh, setup_s = build_workload(args.config, args.scale)
     C, E = mesh.n_cells, mesh.n_edges
@@ -302,7 +376,7 @@ def run_b200(args):
             traffic = None
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
-           "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": "weak",
+           "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": args.scaling,
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": workload_config(args.config, sc, mesh, world,
                                      {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),

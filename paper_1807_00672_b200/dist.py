@@ -233,7 +233,9 @@ class LocalExchange:
 
 
 class TorchExchange:
-    """One part per rank over torch.distributed (NCCL on GPUs)."""
+    """One part per rank over torch.distributed: NCCL on GPUs (the part's
+    buffers are device tensors), gloo on CPU.  The part provides pack(),
+    unpack(), send_block(i), recv_block(i) and lm (LocalMesh)."""
 
     def __init__(self, part, group=None):
         import torch.distributed as dist
@@ -244,20 +246,22 @@ class TorchExchange:
         p, dist = self.part, self.dist
         p.pack()
         ops = []
-        for i, q in enumerate(p.lm.peers):
-            if p.send_off[i + 1] > p.send_off[i]:
-                ops.append(dist.P2POp(dist.isend, p.send_block(i), q, self.group))
-            if p.recv_off[i + 1] > p.recv_off[i]:
-                ops.append(dist.P2POp(dist.irecv, p.recv_block(i), q, self.group))
+        for i, q in enumerate(p.lm.peers):  # plans are symmetric: both directions per peer
+            sb, rb = p.send_block(i), p.recv_block(i)
+            if sb.numel():
+                ops.append(dist.P2POp(dist.isend, sb, q, self.group))
+            if rb.numel():
+                ops.append(dist.P2POp(dist.irecv, rb, q, self.group))
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
-        torch.cuda.synchronize(p.device)
+        if p.send_buf.is_cuda:
+            torch.cuda.synchronize(p.send_buf.device)
         p.unpack()
 
     def _reduce(self, x, op):
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=torch.device("cuda", self.part.device))
+        t = torch.tensor([x], dtype=torch.float64, device=self.part.send_buf.device)
         self.dist.all_reduce(t, op=op, group=self.group)
         return float(t.item())
 

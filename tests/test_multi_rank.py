@@ -102,6 +102,53 @@ def _free_port():
         return s.getsockname()[1]
 
 
+class OraclePart:
+    """CPU stand-in for dist.PartSolver (same interface), stepping one part
+    with the C oracle -- test infrastructure that lets the product's
+    dist.run_parts / dist.TorchExchange run over gloo on CPU."""
+
+    def __init__(self, lm, state):
+        import torch
+        self.lm, self.co, self.arr = lm, COracle(), local_arrays(lm)
+        self.s = [np.ascontiguousarray(a[lm.cells]) for a in (state.h, state.qx, state.qy)]
+        self.clk = so_clock(0.0, 0, 0.0, 0)
+        ns, nr = sum(map(len, lm.send)), sum(map(len, lm.recv))
+        self.send_buf = torch.zeros(3 * max(1, ns), dtype=torch.float64)
+        self.recv_buf = torch.zeros(3 * max(1, nr), dtype=torch.float64)
+        self.send_off = np.concatenate([[0], np.cumsum([len(x) for x in lm.send])]).astype(int)
+        self.recv_off = np.concatenate([[0], np.cumsum([len(x) for x in lm.recv])]).astype(int)
+
+    def send_block(self, i):
+        return self.send_buf[3 * self.send_off[i]:3 * self.send_off[i + 1]]
+
+    def recv_block(self, i):
+        return self.recv_buf[3 * self.recv_off[i]:3 * self.recv_off[i + 1]]
+
+    def pack(self):
+        cells = np.concatenate(self.lm.send) if self.lm.send else np.zeros(0, int)
+        v = self.send_buf.numpy()[:3 * len(cells)].reshape(-1, 3)
+        for k in range(3):
+            v[:, k] = self.s[k][cells]
+
+    def unpack(self):
+        cells = np.concatenate(self.lm.recv) if self.lm.recv else np.zeros(0, int)
+        v = self.recv_buf.numpy()[:3 * len(cells)].reshape(-1, 3)
+        for k in range(3):
+            self.s[k][cells] = v[:, k]
+
+    def local_cfl(self):
+        dts, ms, bad = self.co.local_cfl(self.arr, self.lm.n_owned, *self.s)
+        assert bad == -1
+        return dts, ms, float(np.sum(self.s[0][:self.lm.n_owned] * self.arr.area[:self.lm.n_owned]))
+
+    def step_global(self, t_end, dts, ms):
+        rc, st = self.co.step_owned(self.arr, self.lm.n_owned, self.s, self.clk, t_end, dts, ms)
+        assert rc == 0
+        n = self.lm.n_owned
+        st.mass = float(np.sum(self.s[0][:n] * self.arr.area[:n]))
+        return st
+
+
 def _gloo_worker(rank, world, port, q):
     import torch
     import torch.distributed as tdist
@@ -111,34 +158,13 @@ def _gloo_worker(rank, world, port, q):
         sc, m = scenario()
         part = dist.partition(m, world)
         lm = dist.local_mesh(m, part, rank)
-
-        def exchange(states):
-            s = states[0]
-            ops, bufs = [], []
-            for i, peer in enumerate(lm.peers):
-                send = torch.from_numpy(np.stack([a[lm.send[i]] for a in s], 1).ravel().copy())
-                recv = torch.empty(3 * len(lm.recv[i]), dtype=torch.float64)
-                ops += [tdist.P2POp(tdist.isend, send, peer), tdist.P2POp(tdist.irecv, recv, peer)]
-                bufs.append((i, recv))
-            for r in tdist.batch_isend_irecv(ops):
-                r.wait()
-            for i, recv in bufs:
-                v = recv.numpy().reshape(-1, 3)
-                for k in range(3):
-                    s[k][lm.recv[i]] = v[:, k]
-
-        def red(x, op):
-            t = torch.tensor([x], dtype=torch.float64)
-            tdist.all_reduce(t, op=op)
-            return float(t.item())
-
-        states, dts = oracle_parts_run(m, sc.state, [lm], 40, exchange,
-                                       lambda x: red(x, tdist.ReduceOp.MIN),
-                                       lambda x: red(x, tdist.ReduceOp.MAX))
+        op = OraclePart(lm, sc.state)
+        recs = dist.run_parts([op], dist.TorchExchange(op), 40)  # the product driver
+        dts = recs[:, 1]
         owned = np.zeros((3, m.n_cells))
         mask = np.zeros(m.n_cells)
         for k in range(3):
-            owned[k][lm.cells[:lm.n_owned]] = states[0][k][:lm.n_owned]
+            owned[k][lm.cells[:lm.n_owned]] = op.s[k][:lm.n_owned]
         mask[lm.cells[:lm.n_owned]] = 1
         t_owned, t_mask = torch.from_numpy(owned), torch.from_numpy(mask)
         tdist.all_reduce(t_owned)  # disjoint ownership: the sum assembles the field
