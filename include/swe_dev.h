@@ -69,7 +69,7 @@ enum {
   SWE_NEGATIVE_DEPTH = 2,  /* compute_fluxes: negative depth at edge N (engine.hpp:168-169) */
   SWE_BLOWUP = 3,          /* advance_step: numeric blowup (engine.hpp:292-297) */
   SWE_CUDA = 4,            /* CUDA runtime failure (message via swe_dev_last_error) */
-  SWE_NCCL = 5,            /* multi-device exchange failure */
+  SWE_NCCL = 5,            /* multi-device exchange failure (a peer did not post in time) */
   SWE_INVALID = 6          /* bad argument / inconsistent mesh view */
 };
 
@@ -163,6 +163,41 @@ SWE_API int swe_dev_local_cfl(swe_dev_ctx* ctx, double* dts, double* max_speed, 
  * dts; max_speed is recorded); rec->mass is the owned mass after the step. */
 SWE_API int swe_dev_step_global(swe_dev_ctx* ctx, double t_end, double dts, double max_speed,
                                 swe_step_record* rec, swe_status* st);
+
+/* ---- linked contexts: the device-resident multi-device step ----
+ * The production multi-GPU path: no host round trip per step.
+ * Each rank's state buffers and a mailbox live in one device allocation (the
+ * arena) that every peer maps.  The step kernel stores the new state of the
+ * owned cells a peer holds as ghosts directly into that peer's next state
+ * buffer over NVLink; the step outcome (CFL bound, max speed, mass, clip
+ * ledger, error) is posted to every rank's mailbox and combined in rank
+ * order, so all ranks commit the same dt sequence, records and ledger, and
+ * the results are bit-identical to one device (the mass is a rank-ordered
+ * sum).  After linking, swe_dev_advance / swe_dev_advance_n_async run the
+ * whole exchange inside the CUDA graph; every rank must make the same calls
+ * (advance, set_state, total_mass are collective).  Error indices of a linked
+ * context are GLOBAL ids (gcell / gedge).  A peer that does not post within
+ * timeout_s yields SWE_NCCL instead of a hang. */
+/* This rank's arena (device pointer) and its CUDA IPC handle (64 bytes). */
+SWE_API int swe_dev_link_export(swe_dev_ctx* ctx, void** arena, unsigned char* ipc_handle);
+/* Link the context as `rank` of `nranks`.  Peers' arenas come either as
+ * pointers valid in this process (arenas[q], contexts of this process, same
+ * or peer-enabled devices) or as IPC handles (ipc_handles[64*q], other
+ * processes).  peer_cells[q] = n_cells of rank q.  Push entry j sends owned
+ * cell push_cell[j] (reference-local id) to ghost push_ghost[j] (local id on
+ * rank push_rank[j]).  gcell[C] / gedge[E]: local -> global ids (NULL =
+ * identity). */
+SWE_API int swe_dev_link(swe_dev_ctx* ctx, int rank, int nranks, void* const* arenas,
+                         const unsigned char* ipc_handles, const long long* peer_cells, int n_push,
+                         const int* push_cell, const int* push_rank, const int* push_ghost,
+                         const int* gcell, const int* gedge, double timeout_s);
+/* One phase of a linked single step, enqueued only (lockstep driving of
+ * several linked contexts from one thread, e.g. parts sharing one device):
+ * 0 open, 1 CFL wait + gate, 2 step kernel + halo push, 3 post, 4 wait +
+ * commit.  Run phase k on every context before phase k+1 on any. */
+SWE_API int swe_dev_link_phase(swe_dev_ctx* ctx, int phase, double t_end);
+/* Status and record of the last single step (after phase 4). */
+SWE_API int swe_dev_last_record(swe_dev_ctx* ctx, swe_step_record* rec, swe_status* st);
 
 /* Kernel-level timing: when enabled, swe_dev_advance_n_async launches without
  * a graph and brackets every kernel with CUDA events; times accumulate per

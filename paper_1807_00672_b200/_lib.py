@@ -78,6 +78,11 @@ _SIGS = {
                                   C.POINTER(swe_status)]),
     "swe_dev_step_global": (c_int, [c_void_p, c_double, c_double, c_double,
                                     C.POINTER(swe_step_record), C.POINTER(swe_status)]),
+    "swe_dev_link_export": (c_int, [c_void_p, C.POINTER(c_void_p), c_void_p]),
+    "swe_dev_link": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, c_void_p, c_int,
+                             c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double]),
+    "swe_dev_link_phase": (c_int, [c_void_p, c_int, c_double]),
+    "swe_dev_last_record": (c_int, [c_void_p, C.POINTER(swe_step_record), C.POINTER(swe_status)]),
     "swe_dev_stream": (c_void_p, [c_void_p]),
     "swe_dev_memory_bytes": (c_ll, [c_void_p]),
     "swe_dev_launch_count": (c_ll, []),

@@ -48,13 +48,59 @@ struct Ctl {
   int bad_edge;
   int bad_cell;
   int bad_speed;
-  int pad;
+  int link_err;  // a peer exchange timed out (sticky until set_state)
+  unsigned long long xseq;  // exchanges posted so far (linked contexts)
 };
 
 struct Part {  // one block's partial results
   double lo, hi, mass, clip;
   long long events;
   long long pad;
+};
+
+// ---------------------------------------------------------------------------
+// Linked contexts (multi-device).  Every rank's state arrays and
+// mailbox live in one device allocation (the arena) that its peers map (CUDA
+// IPC across processes, plain pointers within one).  Per step:
+//   k_tile   pushes the new state of the owned cells a peer holds as ghosts
+//            straight into that peer's next state buffer (P2P stores);
+//   k_post   posts the rank's step outcome (reduced CFL bound, speed, mass,
+//            clip ledger, error) into every rank's mailbox slot, then
+//            releases a flag;
+//   k_wait   acquires all ranks' flags and combines the posts in rank order,
+//            so every rank commits the same global dt, record and ledger.
+// No host round trip: the whole loop stays in the CUDA graph.
+// ---------------------------------------------------------------------------
+constexpr int kMaxRanks = 64;
+
+struct XPost {  // one rank's contribution to one exchange
+  double lo, hi, mass, clip;
+  long long events;
+  unsigned long long tag;
+  int status;     // local outcome of the step
+  int index;      // global id of the offending edge / cell
+  int bad_speed;  // global id of the lowest cell with a non-finite speed, or kNone
+  int pad;
+  double err_h;   // depth of the blown-up cell (BLOWUP)
+};
+
+struct Mailbox {
+  unsigned long long flag[kMaxRanks];  // flag[q]: last tag rank q posted here
+  XPost slot[2][kMaxRanks];            // [tag & 1][q]
+};
+
+struct Link {
+  int rank, nranks;  // nranks == 0: not linked
+  Mailbox* mine;
+  Mailbox* const* box;        // [nranks] every rank's mailbox, mapped here
+  double* const* state;       // [6 * nranks] h0 qx0 qy0 h1 qx1 qy1 of every rank
+  const int* tile_push;       // [ntiles + 1] push-list range of each tile
+  const int* push_cell;       // device cell of each push entry (sorted)
+  const int* push_rank;       // destination rank
+  const int* push_ghost;      // ghost cell id on the destination rank
+  const int* gcell;           // reference-local cell -> global id
+  const int* gedge;           // reference-local edge -> global id
+  unsigned long long timeout_ns;
 };
 
 struct Dev {
@@ -90,7 +136,24 @@ struct Dev {
   Part* part;
   swe_step_record* rec;
   Phys P;
+  Link L;
 };
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // engine.hpp:236-237
 __device__ __forceinline__ double step_dt(const Ctl* c, double t_end, bool* last_out) {
@@ -220,38 +283,31 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
     c->err_index = c->cfl_bad;
     go = 0;
   }
+  if (go && sp->mode != 2 && c->link_err) {
+    c->status = SWE_NCCL;
+    c->err_index = -1;
+    go = 0;
+  }
   c->active = go;
   if (use_cond) cudaGraphSetConditional(cond, go);
 }
 
-// finalize: engine.hpp:292-307 + the fused CFL cache for the next step;
-// n = number of partials the step kernel wrote
-__global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
-                                                     int use_cond) {
+// engine.hpp:292-307 + the fused CFL cache for the next step, given the
+// step's reduced partials p and outcome (status, index, err_h); thread 0 only
+__device__ void finalize_step(const Dev& d, const Part& p, int status, int index, double err_h,
+                              cudaGraphConditionalHandle cond, int use_cond) {
   Ctl* c = d.ctl;
-  if (!c->active) {
-    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
-    return;
-  }
-  const Part p = reduce_parts(d, n);
-  if (threadIdx.x != 0) return;
   const StepParams* sp = d.sp;
   bool last;
   const double dt = step_dt(c, sp->t_end, &last);
-  int go = 1;
-  if (c->bad_edge != kNone) {  // engine.hpp:168-169
-    c->status = SWE_NEGATIVE_DEPTH;
-    c->err_index = c->bad_edge;
-    go = 0;
-  } else if (c->bad_cell != kNone) {  // engine.hpp:292-297; state is not committed
-    c->status = SWE_BLOWUP;
-    c->err_index = c->bad_cell;
-    c->err_step = c->step;
-    c->err_dt = dt;
-    c->err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
-    go = 0;
-  }
-  if (!go) {
+  if (status != SWE_OK) {  // engine.hpp:168-169, :292-297; state is not committed
+    c->status = status;
+    c->err_index = index;
+    if (status == SWE_BLOWUP) {
+      c->err_step = c->step;
+      c->err_dt = dt;
+      c->err_h = err_h;
+    }
     c->bad_edge = kNone;
     c->bad_cell = kNone;
     c->bad_speed = kNone;
@@ -279,8 +335,8 @@ __global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphCond
   c->n_rec += 1;
   set_cfl_cache(c, p, d.P);
   // continue? (engine.hpp:355-358, :374-375)
-  go = c->t < sp->t_end && c->step < sp->max_steps && !(c->t >= sp->next_snap - 1e-12) &&
-       (sp->ring || c->n_rec < sp->rec_cap);
+  int go = c->t < sp->t_end && c->step < sp->max_steps && !(c->t >= sp->next_snap - 1e-12) &&
+           (sp->ring || c->n_rec < sp->rec_cap);
   if (go && c->cfl_bad != kNone) {
     c->status = SWE_NONFINITE_SPEED;
     c->err_index = c->cfl_bad;
@@ -288,6 +344,123 @@ __global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphCond
   }
   c->active = go;
   if (use_cond) cudaGraphSetConditional(cond, go);
+}
+
+// finalize of a single-domain step; n = number of partials the step kernel wrote
+__global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
+                                                     int use_cond) {
+  Ctl* c = d.ctl;
+  if (!c->active) {
+    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x != 0) return;
+  int status = SWE_OK, index = kNone;
+  double err_h = 0.0;
+  if (c->bad_edge != kNone) {  // engine.hpp:168-169
+    status = SWE_NEGATIVE_DEPTH;
+    index = c->bad_edge;
+  } else if (c->bad_cell != kNone) {  // engine.hpp:292-297
+    status = SWE_BLOWUP;
+    index = c->bad_cell;
+    err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
+  }
+  finalize_step(d, p, status, index, err_h, cond, use_cond);
+}
+
+// ---- linked contexts: post / wait (see Link) ------------------------------
+// kind 0: a step's outcome (partials of the step kernel, error slots);
+// kind 1: the CFL bound of the current state (partials of k_cfl)
+__global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
+  Ctl* c = d.ctl;
+  if (kind == 0 && !c->active) return;
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x != 0) return;
+  const Link& L = d.L;
+  XPost x;
+  x.lo = p.lo;
+  x.hi = p.hi;
+  x.mass = p.mass;
+  x.clip = p.clip;
+  x.events = p.events;
+  x.status = SWE_OK;
+  x.index = kNone;
+  x.err_h = 0.0;
+  x.pad = 0;
+  if (kind == 0 && c->bad_edge != kNone) {
+    x.status = SWE_NEGATIVE_DEPTH;
+    x.index = L.gedge[c->bad_edge];
+  } else if (kind == 0 && c->bad_cell != kNone) {
+    x.status = SWE_BLOWUP;
+    x.index = L.gcell[c->bad_cell];
+    x.err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
+  }
+  x.bad_speed = c->bad_speed == kNone ? kNone : L.gcell[c->bad_speed];
+  c->bad_edge = kNone;
+  c->bad_cell = kNone;
+  c->bad_speed = kNone;
+  const unsigned long long tag = ++c->xseq;
+  x.tag = tag;
+  for (int q = 0; q < L.nranks; ++q) L.box[q]->slot[tag & 1][L.rank] = x;
+  __threadfence_system();
+  for (int q = 0; q < L.nranks; ++q) st_release_sys(&L.box[q]->flag[L.rank], tag);
+}
+
+__global__ void k_wait(Dev d, int kind, cudaGraphConditionalHandle cond, int use_cond) {
+  Ctl* c = d.ctl;
+  if (kind == 0 && !c->active) {
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const Link& L = d.L;
+  const unsigned long long tag = c->xseq;
+  Mailbox* m = L.mine;
+  const unsigned long long t0 = global_ns();
+  bool timeout = false;
+  for (int q = 0; q < L.nranks && !timeout; ++q)
+    while (ld_acquire_sys(&m->flag[q]) < tag) {
+      if (global_ns() - t0 > L.timeout_ns) {
+        timeout = true;
+        break;
+      }
+      __nanosleep(100);
+    }
+  // combine in rank order: every rank forms the same sums
+  Part g{INFINITY, 0.0, 0.0, 0.0, 0, 0};
+  int neg = kNone, blow = kNone, bad = kNone;
+  double err_h = 0.0;
+  for (int q = 0; q < L.nranks && !timeout; ++q) {
+    const volatile XPost* s = &m->slot[tag & 1][q];
+    if (s->tag != tag) timeout = true;  // a post from a different exchange
+    g.lo = sel_min(g.lo, s->lo);
+    g.hi = sel_max(g.hi, s->hi);
+    g.mass += s->mass;
+    g.clip += s->clip;
+    g.events += s->events;
+    if (s->status == SWE_NEGATIVE_DEPTH) neg = min(neg, s->index);
+    if (s->status == SWE_BLOWUP && s->index < blow) {
+      blow = s->index;
+      err_h = s->err_h;
+    }
+    bad = min(bad, s->bad_speed);
+  }
+  if (timeout) {
+    c->link_err = 1;
+    c->status = SWE_NCCL;
+    c->err_index = -1;
+    c->active = 0;
+    c->cfl_valid = 0;
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  c->bad_speed = bad;
+  if (kind == 1) {
+    set_cfl_cache(c, g, d.P);
+    return;
+  }
+  const int status = neg != kNone ? SWE_NEGATIVE_DEPTH : (blow != kNone ? SWE_BLOWUP : SWE_OK);
+  finalize_step(d, g, status, status == SWE_NEGATIVE_DEPTH ? neg : blow, err_h, cond, use_cond);
 }
 
 }  // namespace swe_b200

@@ -47,6 +47,14 @@ bool cuda_ok(cudaError_t e, const char* what) {
 
 int blocks_for(long long n, int b = kBlock) { return (int)((n + b - 1) / b); }
 
+// arena layout: [Mailbox][h0][qx0][qy0][h1][qx1][qy1], 256-byte aligned;
+// arena_offset(C, k) = byte offset of state array k (k = 6: total size)
+size_t arena_offset(long long C, int k) {
+  const size_t box = (sizeof(Mailbox) + 255) & ~(size_t)255;
+  const size_t arr = ((size_t)C * sizeof(double) + 255) & ~(size_t)255;
+  return box + (size_t)k * arr;
+}
+
 int fail_invalid(const char* msg) {
   g_last_error = msg;
   return SWE_INVALID;
@@ -76,6 +84,13 @@ struct swe_dev_ctx {
   size_t tile_smem = 0;
   int max_slots = 0;  // most edges (owned + halo) one tile evaluates
   long long n_halo = 0;
+  // linked contexts (multi-device)
+  char* arena = nullptr;  // mailbox + state arrays, mapped by the peers
+  size_t arena_bytes = 0;
+  bool linked = false;
+  bool cfl_posted = false;  // link_phase: a CFL exchange awaits its wait
+  std::vector<void*> link_allocs;  // device tables of the link
+  std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -95,26 +110,57 @@ struct swe_dev_ctx {
     return static_cast<V*>(p);
   }
   int n_step_parts() const { return fused ? grid_tile : grid_cell; }
+  int n_push = 0;
 };
 
 namespace {
 
-int launch_update(swe_dev_ctx* x) {  // the step kernel(s) before finalize, 1 or 2 launches
+const void* tile_kernel(int threads, bool link) {
+  if (threads == 128) return link ? (const void*)k_tile<128, true> : (const void*)k_tile<128, false>;
+  return link ? (const void*)k_tile<256, true> : (const void*)k_tile<256, false>;
+}
+
+int launch_update(swe_dev_ctx* x) {  // the step kernel(s) before finalize
   if (x->fused) {
-    if (x->tile_threads == 128)
-      k_tile<128><<<x->grid_tile, 128, x->tile_smem, x->stream>>>(x->d);
-    else
-      k_tile<256><<<x->grid_tile, 256, x->tile_smem, x->stream>>>(x->d);
+    const bool L = x->linked;
+    if (x->tile_threads == 128) {
+      if (L) k_tile<128, true><<<x->grid_tile, 128, x->tile_smem, x->stream>>>(x->d);
+      else k_tile<128, false><<<x->grid_tile, 128, x->tile_smem, x->stream>>>(x->d);
+    } else {
+      if (L) k_tile<256, true><<<x->grid_tile, 256, x->tile_smem, x->stream>>>(x->d);
+      else k_tile<256, false><<<x->grid_tile, 256, x->tile_smem, x->stream>>>(x->d);
+    }
     ++g_launches;
     return cuda_ok(cudaGetLastError(), "k_tile") ? SWE_OK : SWE_CUDA;
   }
   k_face_c<<<x->grid_face, kBlock, 0, x->stream>>>(x->d);
   k_cell_c<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
   g_launches += 2;
+  if (x->linked) {
+    k_push<<<blocks_for(std::max(1, x->n_push)), kBlock, 0, x->stream>>>(x->d);
+    ++g_launches;
+  }
   return cuda_ok(cudaGetLastError(), "k_face_c/k_cell_c") ? SWE_OK : SWE_CUDA;
 }
 
+// linked: post this rank's outcome / CFL bound, then wait for every rank's
+int launch_post(swe_dev_ctx* x, int n, int kind) {
+  k_post<<<1, kBlock, 0, x->stream>>>(x->d, n, kind);
+  ++g_launches;
+  return cuda_ok(cudaGetLastError(), "k_post") ? SWE_OK : SWE_CUDA;
+}
+
+int launch_wait(swe_dev_ctx* x, int kind, cudaGraphConditionalHandle h, int use_cond) {
+  k_wait<<<1, 1, 0, x->stream>>>(x->d, kind, h, use_cond);
+  ++g_launches;
+  return cuda_ok(cudaGetLastError(), "k_wait") ? SWE_OK : SWE_CUDA;
+}
+
 int launch_finalize(swe_dev_ctx* x, cudaGraphConditionalHandle h, int use_cond) {
+  if (x->linked) {
+    if (int rc = launch_post(x, x->n_step_parts(), 0)) return rc;
+    return launch_wait(x, 0, h, use_cond);
+  }
   k_finalize<<<1, kBlock, 0, x->stream>>>(x->d, x->n_step_parts(), h, use_cond);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_finalize") ? SWE_OK : SWE_CUDA;
@@ -137,8 +183,13 @@ int ensure_cfl(swe_dev_ctx* x, bool force = false) {
   if (int rc = sync_ctl(x)) return rc;
   if (x->h_ctl->cfl_valid && !force) return SWE_OK;
   k_cfl<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
+  ++g_launches;
+  if (x->linked) {  // the global bound: every rank posts, then waits
+    if (int rc = launch_post(x, x->grid_cell, 1)) return rc;
+    return launch_wait(x, 1, cudaGraphConditionalHandle{}, 0);
+  }
   k_prepare<<<1, kBlock, 0, x->stream>>>(x->d, x->grid_cell);
-  g_launches += 2;
+  ++g_launches;
   CK(cudaGetLastError());
   return SWE_OK;
 }
@@ -466,11 +517,19 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.halo = x->alloc<int>(E);
   d.kl = x->alloc<unsigned char>(E);
   d.kr = x->alloc<unsigned char>(E);
-  for (int b = 0; b < 2; ++b) {
-    d.h[b] = x->alloc<double>(C);
-    d.qx[b] = x->alloc<double>(C);
-    d.qy[b] = x->alloc<double>(C);
+  // state arrays + mailbox in one allocation (the arena peers map)
+  x->arena_bytes = arena_offset(C, 6);
+  x->arena = x->alloc<char>(x->arena_bytes);
+  if (!x->arena) {
+    g_last_error = "swe_dev_create: cudaMalloc failed";
+    return bail(SWE_CUDA);
   }
+  for (int b = 0; b < 2; ++b) {
+    d.h[b] = (double*)(x->arena + arena_offset(C, 3 * b));
+    d.qx[b] = (double*)(x->arena + arena_offset(C, 3 * b + 1));
+    d.qy[b] = (double*)(x->arena + arena_offset(C, 3 * b + 2));
+  }
+  d.L.mine = (Mailbox*)x->arena;
   // edge records: compute_fluxes (engine.hpp:138-170)
   d.M = x->alloc<double>(E);
   d.LX = x->alloc<double>(E);
@@ -518,11 +577,13 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
                    std::to_string(smem_optin) + "); use a smaller SWE_TILE_CELLS";
     return bail(SWE_INVALID);
   }
-  const void* ktile = x->tile_threads == 128 ? (const void*)k_tile<128> : (const void*)k_tile<256>;
-  if (!cuda_ok(cudaFuncSetAttribute(ktile, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)x->tile_smem),
-               "tile smem attribute"))
-    return bail(SWE_CUDA);
+  const void* ktile = tile_kernel(x->tile_threads, false);
+  for (int L = 0; L < 2; ++L)
+    if (!cuda_ok(cudaFuncSetAttribute(tile_kernel(x->tile_threads, L),
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)x->tile_smem),
+                 "tile smem attribute"))
+      return bail(SWE_CUDA);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tile, ktile, x->tile_threads, x->tile_smem);
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
@@ -539,11 +600,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   cudaStream_t s = x->stream;
   if (!cuda_ok(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s), "ctl"))
     return bail(SWE_CUDA);
-  for (int b = 0; b < 2; ++b) {
-    cudaMemsetAsync(d.h[b], 0, sizeof(double) * C, s);
-    cudaMemsetAsync(d.qx[b], 0, sizeof(double) * C, s);
-    cudaMemsetAsync(d.qy[b], 0, sizeof(double) * C, s);
-  }
+  cudaMemsetAsync(x->arena, 0, x->arena_bytes, s);  // mailbox flags 0, state 0
   if (!(flags & SWE_FLAG_NO_GRAPH)) {
     const int rc = build_graph(x);
     if (rc != SWE_OK) return bail(rc);
@@ -560,6 +617,8 @@ int swe_dev_destroy(swe_dev_ctx* x) {
   if (x->graph) cudaGraphDestroy(x->graph);
   for (cudaEvent_t e : x->events) cudaEventDestroy(e);
   for (void* p : x->allocs) cudaFree(p);
+  for (void* p : x->link_allocs) cudaFree(p);
+  for (void* p : x->ipc_mapped) cudaIpcCloseMemHandle(p);
   cudaFree(x->halo_send);
   cudaFree(x->halo_recv);
   if (x->h_ctl) cudaFreeHost(x->h_ctl);
@@ -591,6 +650,7 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
   c.status = SWE_OK;
   c.active = 0;
   c.bad_edge = c.bad_cell = c.bad_speed = kNone;
+  c.link_err = 0;
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -930,6 +990,173 @@ int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
                            x->d.E};
   for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];
   return SWE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// linked contexts (multi-device); see Link in swe_ctl.cuh
+// ---------------------------------------------------------------------------
+int swe_dev_link_export(swe_dev_ctx* x, void** arena, unsigned char* ipc_handle) {
+  if (!x) return fail_invalid("null context");
+  if (arena) *arena = x->arena;
+  if (ipc_handle) {
+    CK(cudaSetDevice(x->device));
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, x->arena));
+    std::memcpy(ipc_handle, &h, sizeof(h));
+  }
+  return SWE_OK;
+}
+
+int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
+                 const unsigned char* ipc_handles, const long long* peer_cells, int n_push,
+                 const int* push_cell, const int* push_rank, const int* push_ghost,
+                 const int* gcell, const int* gedge, double timeout_s) {
+  if (!x) return fail_invalid("null context");
+  if (x->linked) return fail_invalid("swe_dev_link: context is already linked");
+  if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !peer_cells ||
+      (!arenas && !ipc_handles) || n_push < 0 ||
+      (n_push && (!push_cell || !push_rank || !push_ghost)))
+    return fail_invalid("swe_dev_link: bad argument");
+  Dev& d = x->d;
+  if (peer_cells[rank] != d.C) return fail_invalid("swe_dev_link: peer_cells[rank] != n_cells");
+  for (int j = 0; j < n_push; ++j) {
+    const int q = push_rank[j];
+    if (push_cell[j] < 0 || push_cell[j] >= d.C_own || q < 0 || q >= nranks || q == rank ||
+        push_ghost[j] < 0 || push_ghost[j] >= peer_cells[q])
+      return fail_invalid("swe_dev_link: bad push entry");
+  }
+  CK(cudaSetDevice(x->device));
+  // peers' arenas in this process
+  std::vector<char*> base(nranks, nullptr);
+  for (int q = 0; q < nranks; ++q) {
+    if (q == rank) {
+      base[q] = x->arena;
+    } else if (arenas) {
+      base[q] = (char*)arenas[q];
+      cudaPointerAttributes a{};
+      CK(cudaPointerGetAttributes(&a, base[q]));
+      if (a.device != x->device) {  // another device of this process
+        const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else CK(e);
+      }
+    } else {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, ipc_handles + sizeof(h) * q, sizeof(h));
+      void* p = nullptr;
+      CK(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+      x->ipc_mapped.push_back(p);
+      base[q] = (char*)p;
+    }
+  }
+  std::vector<Mailbox*> boxes(nranks);
+  std::vector<double*> states(6 * (size_t)nranks);
+  for (int q = 0; q < nranks; ++q) {
+    boxes[q] = (Mailbox*)base[q];
+    for (int k = 0; k < 6; ++k) states[6 * q + k] = (double*)(base[q] + arena_offset(peer_cells[q], k));
+  }
+  // push list in device cell order, grouped by tile
+  std::vector<int> c_new(d.C);
+  CK(cudaMemcpy(c_new.data(), d.c_new, sizeof(int) * d.C, cudaMemcpyDeviceToHost));
+  std::vector<int> order(n_push);
+  for (int j = 0; j < n_push; ++j) order[j] = j;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) {
+    return c_new[push_cell[a]] < c_new[push_cell[b]];
+  });
+  std::vector<int> pc(std::max(1, n_push)), pr(std::max(1, n_push)), pg(std::max(1, n_push));
+  std::vector<int> tp(d.ntiles + 1, 0);
+  for (int j = 0; j < n_push; ++j) {
+    const int o = order[j];
+    pc[j] = c_new[push_cell[o]];
+    pr[j] = push_rank[o];
+    pg[j] = push_ghost[o];  // ghosts keep their local ids on the device
+    ++tp[pc[j] / d.T + 1];
+  }
+  for (int t = 0; t < d.ntiles; ++t) tp[t + 1] += tp[t];
+  std::vector<int> gc(d.C), ge(d.E);
+  for (int c = 0; c < d.C; ++c) gc[c] = gcell ? gcell[c] : c;
+  for (int e = 0; e < d.E; ++e) ge[e] = gedge ? gedge[e] : e;
+  auto upload = [&](const void* src, size_t bytes) -> void* {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes) != cudaSuccess) return nullptr;
+    x->link_allocs.push_back(p);
+    if (cudaMemcpy(p, src, bytes, cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    return p;
+  };
+  Link L{};
+  L.rank = rank;
+  L.nranks = nranks;
+  L.mine = (Mailbox*)x->arena;
+  L.box = (Mailbox* const*)upload(boxes.data(), sizeof(Mailbox*) * nranks);
+  L.state = (double* const*)upload(states.data(), sizeof(double*) * states.size());
+  L.tile_push = (const int*)upload(tp.data(), sizeof(int) * tp.size());
+  L.push_cell = (const int*)upload(pc.data(), sizeof(int) * pc.size());
+  L.push_rank = (const int*)upload(pr.data(), sizeof(int) * pr.size());
+  L.push_ghost = (const int*)upload(pg.data(), sizeof(int) * pg.size());
+  L.gcell = (const int*)upload(gc.data(), sizeof(int) * gc.size());
+  L.gedge = (const int*)upload(ge.data(), sizeof(int) * ge.size());
+  L.timeout_ns = (unsigned long long)((timeout_s > 0 ? timeout_s : 60.0) * 1e9);
+  if (!L.box || !L.state || !L.tile_push || !L.push_cell || !L.push_rank || !L.push_ghost ||
+      !L.gcell || !L.gedge) {
+    g_last_error = "swe_dev_link: device tables: " + std::string(cudaGetErrorString(cudaGetLastError()));
+    return SWE_CUDA;
+  }
+  d.L = L;
+  x->n_push = n_push;
+  x->linked = true;
+  // the CFL cache must be re-formed globally; the graph gains the exchange
+  if (int rc = sync_ctl(x)) return rc;
+  x->h_ctl->cfl_valid = 0;
+  CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, x->stream));
+  if (x->exec) {
+    CK(cudaGraphExecDestroy(x->exec));
+    CK(cudaGraphDestroy(x->graph));
+    x->exec = nullptr;
+    x->graph = nullptr;
+    if (int rc = build_graph(x)) return rc;
+  }
+  CK(cudaStreamSynchronize(x->stream));
+  return SWE_OK;
+}
+
+// One phase of a linked step, enqueued without waiting, so that a single
+// host thread can drive several linked contexts sharing one device in
+// lockstep (every rank's post is enqueued before any rank's wait):
+//   0 open (local CFL bound + post if stale)  1 CFL wait + gate
+//   2 step kernel(s) + halo push               3 post the step outcome
+//   4 wait, combine, commit
+int swe_dev_link_phase(swe_dev_ctx* x, int phase, double t_end) {
+  if (!x) return fail_invalid("null context");
+  if (!x->linked) return fail_invalid("swe_dev_link_phase: context is not linked");
+  switch (phase) {
+    case 0: {
+      if (int rc = sync_ctl(x)) return rc;
+      x->cfl_posted = !x->h_ctl->cfl_valid;
+      if (x->cfl_posted) {
+        k_cfl<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
+        ++g_launches;
+        if (int rc = launch_post(x, x->grid_cell, 1)) return rc;
+      }
+      return write_params(x, t_end, LLONG_MAX, INFINITY, 1, 0, 1);
+    }
+    case 1:
+      if (x->cfl_posted)
+        if (int rc = launch_wait(x, 1, cudaGraphConditionalHandle{}, 0)) return rc;
+      x->cfl_posted = false;
+      return launch_gate(x);
+    case 2: return launch_update(x);
+    case 3: return launch_post(x, x->n_step_parts(), 0);
+    case 4: return launch_wait(x, 0, cudaGraphConditionalHandle{}, 0);
+  }
+  return fail_invalid("swe_dev_link_phase: phase must be 0..4");
+}
+
+int swe_dev_last_record(swe_dev_ctx* x, swe_step_record* rec, swe_status* st) {
+  if (!x) return fail_invalid("null context");
+  const int code = read_status(x, st);
+  if (code == SWE_OK && rec && x->h_ctl->n_rec > 0)
+    CK(cudaMemcpy(rec, x->rec, sizeof(swe_step_record), cudaMemcpyDeviceToHost));
+  return code;
 }
 
 void* swe_dev_stream(swe_dev_ctx* x) { return x ? (void*)x->stream : nullptr; }

@@ -80,7 +80,7 @@ __device__ __forceinline__ bool edge_terms(const Cons& uL, double zl, const Cons
 // engine.hpp:265-289 given the cell's summed fluxes and its area / Manning n /
 // inradius; writes the new state and accumulates the clip ledger, the mass
 // and the next step's CFL bound
-__device__ __forceinline__ void cell_finish_v(const Dev& d, int c, double h, double qx, double qy,
+__device__ __forceinline__ Cons cell_finish_v(const Dev& d, int c, double h, double qx, double qy,
                                               double am, double ax, double ay, double dt,
                                               double area, double man, double inr, double* NH,
                                               double* NQX, double* NQY, CellAcc& a) {
@@ -93,7 +93,7 @@ __device__ __forceinline__ void cell_finish_v(const Dev& d, int c, double h, dou
     NH[c] = u.h;
     NQX[c] = u.qx;
     NQY[c] = u.qy;
-    return;
+    return u;
   }
   if (u.h < 0.0) {  // clamp_dry, kernels.hpp:205-216
     a.clip += (-u.h) * area;
@@ -115,12 +115,13 @@ __device__ __forceinline__ void cell_finish_v(const Dev& d, int c, double h, dou
       a.hi = sel_max(a.hi, s);
     }
   }
+  return u;
 }
 
-__device__ __forceinline__ void cell_finish(const Dev& d, int c, double h, double qx, double qy,
+__device__ __forceinline__ Cons cell_finish(const Dev& d, int c, double h, double qx, double qy,
                                             double am, double ax, double ay, double dt,
                                             double* NH, double* NQX, double* NQY, CellAcc& a) {
-  cell_finish_v(d, c, h, qx, qy, am, ax, ay, dt, __ldg(d.area + c), __ldg(d.man + c),
+  return cell_finish_v(d, c, h, qx, qy, am, ax, ay, dt, __ldg(d.area + c), __ldg(d.man + c),
                 __ldg(d.inr + c), NH, NQX, NQY, a);
 }
 
@@ -229,6 +230,22 @@ __global__ void __launch_bounds__(kBlock, SWE_CELL_MINB) k_cell_c(Dev d) {
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
 }
 
+// linked two-phase step: push the new state of the cells peers hold as ghosts
+__global__ void __launch_bounds__(kBlock) k_push(Dev d) {
+  const Ctl* ctl = d.ctl;
+  if (!ctl->active) return;
+  const int nxt = ctl->cur ^ 1;
+  const int n = d.L.tile_push[d.ntiles];
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int c = d.L.push_cell[j], g = d.L.push_ghost[j];
+  double* const* dst = d.L.state + 6 * d.L.push_rank[j] + 3 * nxt;
+  dst[0][g] = d.h[nxt][c];
+  dst[1][g] = d.qx[nxt][c];
+  dst[2][g] = d.qy[nxt][c];
+  __threadfence_system();
+}
+
 // ---------------------------------------------------------------------------
 // fused tile kernel.  Per tile of T Morton-consecutive cells: stage the
 // tile's state and bed in shared memory, evaluate the owned + halo edges into per-incidence contributions in shared
@@ -242,7 +259,9 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
   return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;
 }
 
-template <int NT>
+// LINK: linked context -- after the update, push the tile's cells that peers
+// hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh)
+template <int NT, bool LINK>
 __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   extern __shared__ double smem[];
   Ctl* ctl = d.ctl;
@@ -333,9 +352,26 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
         ax += tx[3 * i + k];
         ay += ty[3 * i + k];
       }
-      cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
+      const Cons u = cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
+      if (LINK) {  // the tile's new state, for the push below
+        sh[i] = u.h;
+        sq[i] = u.qx;
+        sr[i] = u.qy;
+      }
     }
     __syncthreads();
+    if (LINK) {
+      const int p0 = __ldg(d.L.tile_push + t), p1 = __ldg(d.L.tile_push + t + 1);
+      for (int j = p0 + threadIdx.x; j < p1; j += NT) {
+        const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);
+        double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + j) + 3 * (cur ^ 1);
+        dst[0][g] = sh[i];
+        dst[1][g] = sq[i];
+        dst[2][g] = sr[i];
+      }
+      if (p1 > p0) __threadfence_system();
+      __syncthreads();
+    }
   }
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
 }

@@ -275,6 +275,202 @@ class TorchExchange:
         return self._reduce(x, self.dist.ReduceOp.SUM)
 
 
+# ---------------------------------------------------------------------------
+# Linked contexts: the device-resident multi-device step (include/swe_dev.h
+# "linked contexts").  Ghost states are pushed peer-to-peer by the step
+# kernel and the CFL bound / step outcome is exchanged through device
+# mailboxes, so a run is one CUDA graph launch per rank with no host round
+# trip per step.
+# ---------------------------------------------------------------------------
+def push_plan(lm: LocalMesh, peer_recv: dict):
+    """Push entries of part lm.part: (owned local cell, destination rank,
+    ghost local id on that rank).  peer_recv[q] = (q's peers, q's recv lists);
+    plans are symmetric -- lm.send[i] and q's recv list for lm.part hold the
+    same global cells in the same order."""
+    cells, ranks, ghosts = [], [], []
+    for i, q in enumerate(lm.peers):
+        qpeers, qrecv = peer_recv[q]
+        j = list(qpeers).index(lm.part)
+        s, r = np.asarray(lm.send[i]), np.asarray(qrecv[j])
+        if len(s) != len(r):
+            raise ValueError(f"halo plans of parts {lm.part} and {q} disagree")
+        cells.append(s)
+        ranks.append(np.full(len(s), q))
+        ghosts.append(r)
+    cat = (lambda xs: np.ascontiguousarray(np.concatenate(xs), dtype=np.int32) if xs
+           else np.zeros(0, np.int32))
+    return cat(cells), cat(ranks), cat(ghosts)
+
+
+class LinkedPart:
+    """One part (rank) of a linked multi-device run."""
+
+    def __init__(self, lm: LocalMesh, params: PhysParams = PhysParams(), device: int = 0,
+                 two_phase: bool = False):
+        self.lib = L.load()
+        self.lm, self.params, self.device = lm, params, device
+        v = lm.view()
+        p = params.c()
+        ctx = C.c_void_p()
+        flags = L.SWE_FLAG_TWO_PHASE if two_phase else 0
+        _check(self.lib.swe_dev_create(C.byref(v), C.byref(p), device, flags, C.byref(ctx)),
+               "swe_dev_create(part)")
+        self.ctx = ctx
+        self.linked = False
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.lib.swe_dev_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        self.close()
+
+    def export(self):
+        """(arena device pointer, 64-byte CUDA IPC handle)."""
+        arena = C.c_void_p()
+        h = (C.c_ubyte * 64)()
+        _check(self.lib.swe_dev_link_export(self.ctx, C.byref(arena), h), "swe_dev_link_export")
+        return arena.value, bytes(h)
+
+    def link(self, rank: int, nranks: int, peer_cells, plan, arenas=None, handles=None,
+             timeout_s: float = 60.0):
+        cells, ranks, ghosts = plan
+        pc = np.ascontiguousarray(peer_cells, dtype=np.int64)
+        gc = np.ascontiguousarray(self.lm.cells, dtype=np.int32)
+        ge = np.ascontiguousarray(self.lm.edges, dtype=np.int32)
+        arr = (C.c_void_p * nranks)(*arenas) if arenas is not None else None
+        hnd = (C.c_ubyte * (64 * nranks)).from_buffer_copy(b"".join(handles)) \
+            if handles is not None else None
+        _check(self.lib.swe_dev_link(self.ctx, rank, nranks, arr, hnd, L.ptr(pc), len(cells),
+                                     L.ptr(cells), L.ptr(ranks), L.ptr(ghosts), L.ptr(gc),
+                                     L.ptr(ge), float(timeout_s)), "swe_dev_link")
+        self.linked = True
+
+    def set_state(self, s: FieldState, t=0.0, step=0):
+        """s: GLOBAL state; the part takes its owned + ghost cells."""
+        c = self.lm.cells
+        h, qx, qy = (np.ascontiguousarray(a[c]) for a in (s.h, s.qx, s.qy))
+        _check(self.lib.swe_dev_set_state(self.ctx, L.ptr(h), L.ptr(qx), L.ptr(qy), t, step),
+               "swe_dev_set_state")
+
+    def gather_owned(self, out: FieldState):
+        n = self.lm.n_cells
+        h, qx, qy = np.empty(n), np.empty(n), np.empty(n)
+        t, step = C.c_double(), C.c_longlong()
+        _check(self.lib.swe_dev_get_state(self.ctx, L.ptr(h), L.ptr(qx), L.ptr(qy), C.byref(t),
+                                          C.byref(step)), "swe_dev_get_state")
+        own = self.lm.cells[:self.lm.n_owned]
+        no = self.lm.n_owned
+        out.h[own], out.qx[own], out.qy[own] = h[:no], qx[:no], qy[:no]
+        return t.value, step.value
+
+    def ledger(self):
+        v, n = C.c_double(), C.c_longlong()
+        _check(self.lib.swe_dev_get_ledger(self.ctx, C.byref(v), C.byref(n)), "ledger")
+        return v.value, n.value
+
+    @staticmethod
+    def raise_status(rc, st):
+        """Map a linked status to the reference's exceptions (indices are global)."""
+        if rc == L.SWE_NONFINITE_SPEED:
+            raise NumericError(f"stable_dt: non-finite velocity in cell {st.index}")
+        if rc == L.SWE_NEGATIVE_DEPTH:
+            raise NumericError(f"compute_fluxes: negative depth at edge {st.index}")
+        if rc == L.SWE_BLOWUP:
+            raise NumericError(f"advance_step: numeric blowup at step {st.step}, cell {st.index}, "
+                               f"dt {st.dt:f} (h={st.h:f})")
+        _check(rc, "linked step")
+
+    def advance(self, t_end=1e30, max_steps=1 << 62, next_snapshot=float("inf"),
+                max_records=1 << 16):
+        """run() segment on the device (collective: every rank calls it);
+        returns records (step, t, dt, max_speed, global mass)."""
+        recs = (L.swe_step_record * max_records)()
+        n, st = C.c_longlong(), L.swe_status()
+        rc = self.lib.swe_dev_advance(self.ctx, t_end, max_steps, next_snapshot, recs, max_records,
+                                      C.byref(n), C.byref(st))
+        out = np.array([(r.step, r.t, r.dt, r.max_speed, r.mass) for r in recs[:n.value]],
+                       dtype=np.float64).reshape(-1, 5)
+        if rc:
+            self.raise_status(rc, st)
+        return out
+
+    def advance_async(self, n: int, t_end=float("inf")):
+        _check(self.lib.swe_dev_advance_n_async(self.ctx, n, t_end), "advance_n_async")
+
+    def synchronize(self):
+        st = L.swe_status()
+        rc = self.lib.swe_dev_synchronize(self.ctx, C.byref(st))
+        if rc:
+            self.raise_status(rc, st)
+
+
+def link_local(parts, timeout_s: float = 60.0):
+    """Link the parts of this process (one or several devices)."""
+    nr = len(parts)
+    by_part = {p.lm.part: p for p in parts}
+    if sorted(by_part) != list(range(nr)):
+        raise ValueError("parts must be numbered 0..P-1")
+    arenas = [by_part[q].export()[0] for q in range(nr)]
+    cells = [by_part[q].lm.n_cells for q in range(nr)]
+    recv = {q: (by_part[q].lm.peers, by_part[q].lm.recv) for q in range(nr)}
+    for p in parts:
+        p.link(p.lm.part, nr, cells, push_plan(p.lm, recv), arenas=arenas, timeout_s=timeout_s)
+
+
+def exchange_link_info(part_id: int, lm: LocalMesh, handle: bytes, group=None):
+    """all_gather of every rank's (IPC handle, n_cells, peers, recv lists)."""
+    import torch.distributed as tdist
+    mine = (part_id, handle, lm.n_cells, list(lm.peers), [np.asarray(r).tolist() for r in lm.recv])
+    allv = [None] * tdist.get_world_size(group)
+    tdist.all_gather_object(allv, mine, group=group)
+    allv.sort(key=lambda v: v[0])
+    handles = [v[1] for v in allv]
+    cells = [v[2] for v in allv]
+    recv = {v[0]: (v[3], v[4]) for v in allv}
+    return handles, cells, recv
+
+
+def link_torch(part: LinkedPart, group=None, timeout_s: float = 60.0):
+    """Link one part per rank (torchrun): part id == rank; peers' arenas are
+    mapped through CUDA IPC (NVLink peer memory on one node)."""
+    import torch.distributed as tdist
+    rank, nr = tdist.get_rank(group), tdist.get_world_size(group)
+    if part.lm.part != rank:
+        raise ValueError("link_torch: the part id must equal the rank")
+    _, handle = part.export()
+    handles, cells, recv = exchange_link_info(rank, part.lm, handle, group)
+    part.link(rank, nr, cells, push_plan(part.lm, recv), handles=handles, timeout_s=timeout_s)
+    tdist.barrier(group)
+
+
+def run_lockstep(parts, nsteps: int, t_end: float = 1e30):
+    """Step linked parts of ONE process in lockstep (phase k of every part
+    before phase k+1 of any), e.g. several parts sharing one device.
+    Returns per-step (step, t, dt, max_speed, global mass)."""
+    import torch
+    out = []
+    for _ in range(nsteps):
+        for phase in range(5):
+            for p in parts:
+                _check(p.lib.swe_dev_link_phase(p.ctx, phase, t_end), "swe_dev_link_phase")
+            torch.cuda.synchronize()
+        recs = []
+        for p in parts:
+            rec, st = L.swe_step_record(), L.swe_status()
+            rc = p.lib.swe_dev_last_record(p.ctx, C.byref(rec), C.byref(st))
+            if rc:
+                p.raise_status(rc, st)
+            recs.append((rec.step, rec.t, rec.dt, rec.max_speed, rec.mass))
+        if any(r != recs[0] for r in recs):
+            raise RuntimeError(f"linked parts disagree on the step record: {recs}")
+        out.append(recs[0])
+        if not recs[0][1] < t_end:
+            break
+    return np.array(out, dtype=np.float64).reshape(-1, 5)
+
+
 def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     """nsteps explicit steps of the decomposed domain; returns per-step
     (t, dt, max_speed, mass) with the mass summed over parts in part order."""
@@ -293,4 +489,5 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
 
 
 __all__ = ["partition", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
-           "run_parts", "DeviceError"]
+           "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
+           "run_lockstep", "DeviceError"]

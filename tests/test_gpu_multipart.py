@@ -49,3 +49,82 @@ def test_part_error_reports_global_index():
     p.set_state(st)
     with pytest.raises(api.NumericError, match=f"non-finite velocity in cell {bad}$"):
         p.local_cfl()
+
+
+# ---- linked contexts: the device-resident multi-device step ---------------
+def _scenario_parts(P, scale=0.03, name="sloping_wet_dry"):
+    sc = api.make_scenario(name, scale=scale)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    part = dist.partition(m, P)
+    return sc, m, [dist.local_mesh(m, part, p) for p in range(P)]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4])
+@pytest.mark.parametrize("two_phase", [False, True], ids=["fused", "two_phase"])
+def test_linked_parts_match_single_domain(P, two_phase):
+    """P linked parts on one GPU stepped in lockstep: ghost states pushed by
+    the step kernel, CFL bound / outcome through the device mailboxes."""
+    sc, m, lms = _scenario_parts(P)
+    parts = [dist.LinkedPart(lm, two_phase=two_phase) for lm in lms]
+    dist.link_local(parts)
+    for p in parts:
+        p.set_state(sc.state)
+    recs = dist.run_lockstep(parts, 150)
+    got = api.FieldState.zeros(m.n_cells)
+    for p in parts:
+        t, step = p.gather_owned(got)
+        assert step == 150
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=150)
+    assert bit_equal(recs[:, 2], ref["dts"]) and bit_equal(recs[:, 3], ref["max_speeds"])
+    for k, a in (("h", got.h), ("qx", got.qx), ("qy", got.qy)):
+        assert bit_equal(a, ref[k]), k
+    m0 = float(np.sum(sc.state.h * MeshArrays.from_mesh(m).area))
+    assert abs(recs[-1, 4] - m0) <= 1e-12 * m0 + 1e-9
+    ledgers = [p.ledger() for p in parts]  # the global ledger, on every rank
+    assert all(lg == ledgers[0] for lg in ledgers)
+    assert ledgers[0][1] == ref["clip_events"]
+    assert abs(ledgers[0][0] - ref["clipped_volume"]) <= 1e-12 * max(1.0, ref["clipped_volume"])
+
+
+def test_linked_single_rank_graph_matches_unlinked():
+    """nranks = 1: the exchange (post + wait) runs inside the CUDA graph's
+    WHILE body; results equal the unlinked context bit for bit."""
+    sc, m, lms = _scenario_parts(1)
+    p = dist.LinkedPart(lms[0])
+    dist.link_local([p])
+    p.set_state(sc.state)
+    recs = p.advance(max_steps=200)
+    assert len(recs) == 200
+    solver = api.DeviceSolver(m)
+    solver.set_state(sc.state)
+    ref = solver.advance(1e30, max_steps=200)
+    got = api.FieldState.zeros(m.n_cells)
+    p.gather_owned(got)
+    want, _, _ = solver.get_state()
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), getattr(want, k)), k
+    assert bit_equal(recs[:, 2], ref[:, 2]) and bit_equal(recs[:, 3], ref[:, 3])
+
+
+def test_linked_error_reports_global_index():
+    sc, m, lms = _scenario_parts(2)
+    parts = [dist.LinkedPart(lm) for lm in lms]
+    dist.link_local(parts)
+    st = sc.state.copy()
+    bad = int(lms[1].cells[5])
+    st.h[bad] = 1.0
+    st.qx[bad] = np.nan
+    for p in parts:
+        p.set_state(st)
+    with pytest.raises(api.NumericError, match=f"non-finite velocity in cell {bad}$"):
+        dist.run_lockstep(parts, 1)
+
+
+def test_linked_peer_timeout_is_an_error_not_a_hang():
+    sc, m, lms = _scenario_parts(2)
+    parts = [dist.LinkedPart(lm) for lm in lms]
+    dist.link_local(parts, timeout_s=0.3)
+    parts[0].set_state(sc.state)
+    with pytest.raises(api.DeviceError):
+        parts[0].advance(max_steps=5)  # rank 1 never posts

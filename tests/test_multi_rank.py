@@ -194,3 +194,62 @@ def test_gloo_two_ranks_match_single_domain():
     assert bit_equal(dts, ref["dts"])
     for k, key in enumerate(("h", "qx", "qy")):
         assert bit_equal(field[k], ref[key]), key
+
+
+def test_push_plan_pairs_send_and_recv_lists():
+    """Linked contexts: each push entry carries an owned cell to the ghost
+    slot holding the same global cell on the destination rank."""
+    sc, m = scenario()
+    P = 4
+    part = dist.partition(m, P)
+    lms = [dist.local_mesh(m, part, p) for p in range(P)]
+    recv = {lm.part: (lm.peers, lm.recv) for lm in lms}
+    for lm in lms:
+        cells, ranks, ghosts = dist.push_plan(lm, recv)
+        assert len(cells) == sum(len(s) for s in lm.send)
+        assert np.all(cells < lm.n_owned)
+        for c, q, g in zip(cells, ranks, ghosts):
+            other = lms[q]
+            assert g >= other.n_owned and other.cells[g] == lm.cells[c]
+
+
+def _gloo_link_worker(rank, world, port, q):
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, m = scenario()
+        part = dist.partition(m, world)
+        lm = dist.local_mesh(m, part, rank)
+        handle = bytes([rank]) * 64  # stand-in for the CUDA IPC handle
+        handles, cells, recv = dist.exchange_link_info(rank, lm, handle)
+        plan = dist.push_plan(lm, recv)
+        q.put((rank, handles, cells, [a.tolist() for a in plan]))
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_gloo_link_info_exchange():
+    """The host half of link_torch over 2 gloo ranks: every rank sees all
+    handles / sizes in rank order and builds the same plan as in-process."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_gloo_link_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = dict((r, (h, c, pl)) for r, h, c, pl in (q.get(timeout=300) for _ in range(2)))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    sc, m = scenario()
+    part = dist.partition(m, 2)
+    lms = [dist.local_mesh(m, part, p) for p in range(2)]
+    recv = {lm.part: (lm.peers, lm.recv) for lm in lms}
+    for r in range(2):
+        handles, cells, plan = got[r]
+        assert handles == [bytes([0]) * 64, bytes([1]) * 64]
+        assert cells == [lms[0].n_cells, lms[1].n_cells]
+        want = dist.push_plan(lms[r], recv)
+        assert all(list(a) == b for a, b in zip(want, plan))
