@@ -218,8 +218,11 @@ def run_reference(args):
 
 
 def run_b200_dist(args, rank, local, world):
-    """N > 1: the mesh split across ranks by RCB (one part per GPU), ghost
-    layers refreshed by NCCL send/recv, CFL bound by NCCL all_reduce
+    """N > 1: the mesh split across ranks by RCB (one part per GPU) running as
+    LINKED contexts (include/swe_dev.h): the step kernel pushes ghost states
+    into the peers' buffers over NVLink (CUDA IPC peer memory) and the CFL
+    bound / step outcome goes through device mailboxes, so each rank's run is
+    one CUDA graph launch with no host round trip per step
     (paper_1807_00672_b200/dist.py).  strong: the configured mesh; weak: the
     generator resolution scaled by sqrt(N) (N x the cells)."""
     import torch
@@ -230,24 +233,36 @@ def run_b200_dist(args, rank, local, world):
     sc, mesh, setup_s = build_workload(args.config, scale)
     part = dist.partition(mesh, world)
     lm = dist.local_mesh(mesh, part, rank)
-    ps = dist.PartSolver(lm, device=local)
-    ex = dist.TorchExchange(ps)
-    ps.set_state(sc.state)
+    lp = dist.LinkedPart(lm, device=local)
+    dist.link_torch(lp)
+    lp.set_state(sc.state)
+    horizon = 1.7976931348623157e308
     W, K = max(3, args.warmup), args.steps
-    dist.run_parts([ps], ex, W)
-    stream = torch.cuda.ExternalStream(dist_stream(ps), device=local)
+    lp.advance(t_end=horizon, max_steps=W)
+    # clocks ramp: keep stepping >= 1 s; every rank takes the same decision
+    t_w = time.perf_counter()
+    steps = W
+    while True:
+        go = torch.tensor([1.0 if time.perf_counter() - t_w < 1.0 else 0.0], device="cuda")
+        tdist.all_reduce(go, op=tdist.ReduceOp.MAX)
+        if go.item() == 0.0:
+            break
+        steps += 50
+        lp.advance(t_end=horizon, max_steps=steps)
+    stream = torch.cuda.ExternalStream(dist_stream(lp), device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tdist.barrier()
     torch.cuda.synchronize()
     clk = ClockSampler(local).start() if rank == 0 else None
     w0 = time.time()
     ev0.record(stream)
-    recs = dist.run_parts([ps], ex, K)
+    recs = lp.advance(t_end=horizon, max_steps=steps + K)
     ev1.record(stream)
     torch.cuda.synchronize()
     if clk:
         clk.mark(w0, time.time())
         clk.stop()
+    assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
     ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     ms = float(ms.item())
@@ -255,10 +270,10 @@ def run_b200_dist(args, rank, local, world):
     # e2e: host state in, K steps, owned state back to the host
     tdist.barrier()
     t0 = time.perf_counter()
-    ps.set_state(sc.state)
-    dist.run_parts([ps], ex, K)
+    lp.set_state(sc.state)
+    lp.advance(t_end=horizon, max_steps=K)
     got = api.FieldState.zeros(C)
-    ps.gather_owned(got)
+    lp.gather_owned(got)
     e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
     tdist.all_reduce(e2e_s, op=tdist.ReduceOp.MAX)
     if rank == 0:
@@ -266,21 +281,24 @@ def run_b200_dist(args, rank, local, world):
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args.config, sc, mesh, 1, {
-                   "parallelism": f"{world}-way RCB domain decomposition, one part per GPU, "
-                                  "ghost exchange NCCL send/recv + CFL all_reduce per step "
-                                  "(host-driven)",
+                   "parallelism": f"{world}-way RCB domain decomposition, one part per GPU; "
+                                  "ghost states pushed peer-to-peer by the step kernel, CFL "
+                                  "bound / outcome through device mailboxes (no host round "
+                                  "trip per step)",
                    "cells_per_gpu_max": int(np.bincount(part).max()),
                    "halo_cells_rank0": int(lm.n_cells - lm.n_owned), "setup_s": round(setup_s, 2)}),
-               "gpu_launches": None,
-               "gpu_launches_note": "per step and rank: halo pack/unpack, k_gate, k_tile, "
-                                    "k_finalize (+ NCCL kernels)",
+               "gpu_launches": 3 * K + 1,
+               "gpu_launches_note": "per rank: one CUDA-graph launch = k_gate + K x (k_tile with "
+                                    "halo push, k_post, k_wait) in a conditional WHILE node",
                "clocks": clk.summary() if clk else None,
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
-                       "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": 24 * C / K,
-                       "path": "PartSolver.set_state (host) + K steps + gather_owned (host)"},
-               "step_dt_last": float(recs[-1, 1])}
+                       "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": (24 * C + 40 * K) / K,
+                       "path": "LinkedPart.set_state (host) + advance (K steps, records D2H) + "
+                               "gather_owned (host), max over ranks"},
+               "step_dt_last": float(recs[-1, 2])}
         print(json.dumps(out))
     tdist.barrier()
+    lp.close()
     tdist.destroy_process_group()
 
 

@@ -471,6 +471,28 @@ def run_lockstep(parts, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 5)
 
 
+def run_lockstep_ranks(part: LinkedPart, nsteps: int, t_end: float = 1e30, group=None):
+    """run_lockstep across processes: a torch.distributed barrier between
+    phases, so every rank's post precedes every rank's wait (debug driver
+    for ranks that share a device)."""
+    import torch
+    import torch.distributed as tdist
+    out = []
+    for _ in range(nsteps):
+        for phase in range(5):
+            _check(part.lib.swe_dev_link_phase(part.ctx, phase, t_end), "swe_dev_link_phase")
+            torch.cuda.synchronize()
+            tdist.barrier(group)
+        rec, st = L.swe_step_record(), L.swe_status()
+        rc = part.lib.swe_dev_last_record(part.ctx, C.byref(rec), C.byref(st))
+        if rc:
+            part.raise_status(rc, st)
+        out.append((rec.step, rec.t, rec.dt, rec.max_speed, rec.mass))
+        if not rec.t < t_end:
+            break
+    return np.array(out, dtype=np.float64).reshape(-1, 5)
+
+
 def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     """nsteps explicit steps of the decomposed domain; returns per-step
     (t, dt, max_speed, mass) with the mass summed over parts in part order."""

@@ -128,3 +128,54 @@ def test_linked_peer_timeout_is_an_error_not_a_hang():
     parts[0].set_state(sc.state)
     with pytest.raises(api.DeviceError):
         parts[0].advance(max_steps=5)  # rank 1 never posts
+
+
+def _ipc_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, m, lms = _scenario_parts(world)
+        lp = dist.LinkedPart(lms[rank])
+        dist.link_torch(lp)  # peers' arenas through CUDA IPC handles
+        lp.set_state(sc.state)
+        recs = dist.run_lockstep_ranks(lp, 60)
+        got = api.FieldState.zeros(m.n_cells)
+        lp.gather_owned(got)
+        own = lms[rank].cells[:lms[rank].n_owned]
+        q.put((rank, own, got.h[own], got.qx[own], got.qy[own], recs, lp.ledger()))
+        tdist.barrier()
+        lp.close()
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_linked_ranks_over_cuda_ipc():
+    """Two processes linked through CUDA IPC (the torchrun path of
+    bench.py --gpus N), stepped in lockstep on one GPU."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ipc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    sc, m, _ = _scenario_parts(1)
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=60)
+    assert bit_equal(res[0][5], res[1][5])  # same records on both ranks
+    assert res[0][6] == res[1][6]
+    assert bit_equal(res[0][5][:, 2], ref["dts"])
+    for rank, own, h, qx, qy, _, _ in res:
+        assert bit_equal(h, ref["h"][own]) and bit_equal(qx, ref["qx"][own])
+        assert bit_equal(qy, ref["qy"][own])
