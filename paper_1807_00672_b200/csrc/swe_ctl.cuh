@@ -50,6 +50,8 @@ struct Ctl {
   int bad_speed;
   int link_err;  // a peer exchange timed out (sticky until set_state)
   unsigned long long xseq;  // exchanges posted so far (linked contexts)
+  unsigned int done;        // blocks of the running step kernel that finished
+  int pad2;
 };
 
 struct Part {  // one block's partial results
@@ -222,17 +224,35 @@ __global__ void __launch_bounds__(kBlock) k_cfl(Dev d) {
   block_reduce_part(lo, hi, mass, 0.0, 0, d.part + blockIdx.x);
 }
 
-// fixed-order reduction of n block partials by one block
-__device__ Part reduce_parts(const Dev& d, int n) {
-  __shared__ Part s[kBlock];
+// fixed-order reduction of n block partials by one block; s: blockDim.x
+// Parts of shared scratch.  Loads bypass L1 (the partials were written by
+// other SMs of the same launch when called from a step kernel's last block).
+__device__ Part reduce_parts_into(const Part* part, int n, Part* s) {
   Part p{INFINITY, 0.0, 0.0, 0.0, 0, 0};
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const Part q = d.part[i];
-    p.lo = sel_min(p.lo, q.lo);
-    p.hi = sel_max(p.hi, q.hi);
-    p.mass += q.mass;
-    p.clip += q.clip;
-    p.events += q.events;
+  const int bd = blockDim.x;
+  for (int base = threadIdx.x; base < n; base += 8 * bd) {
+    Part q[8];  // 8 independent loads in flight, folded in index order
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + k * bd;
+      if (i < n) {
+        q[k].lo = __ldcg(&part[i].lo);
+        q[k].hi = __ldcg(&part[i].hi);
+        q[k].mass = __ldcg(&part[i].mass);
+        q[k].clip = __ldcg(&part[i].clip);
+        q[k].events = __ldcg(&part[i].events);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (base + k * bd < n) {
+        p.lo = sel_min(p.lo, q[k].lo);
+        p.hi = sel_max(p.hi, q[k].hi);
+        p.mass += q[k].mass;
+        p.clip += q[k].clip;
+        p.events += q[k].events;
+      }
+    }
   }
   s[threadIdx.x] = p;
   __syncthreads();
@@ -250,6 +270,11 @@ __device__ Part reduce_parts(const Dev& d, int n) {
     __syncthreads();
   }
   return s[0];
+}
+
+__device__ Part reduce_parts(const Dev& d, int n) {
+  __shared__ Part s[kBlock];
+  return reduce_parts_into(d.part, n, s);
 }
 
 __device__ __forceinline__ void set_cfl_cache(Ctl* ctl, const Part& p, const Phys& P) {
@@ -292,91 +317,100 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   if (use_cond) cudaGraphSetConditional(cond, go);
 }
 
+// Ctl through L2 (ld.cg): a step kernel's last block reads fields other
+// blocks of the same launch updated with atomics, and its own SM may hold
+// stale L1 lines of the block from the launch's start
+static_assert(sizeof(Ctl) % 8 == 0, "Ctl is copied as 8-byte words");
+__device__ __forceinline__ Ctl load_ctl(const Ctl* c) {
+  Ctl v;
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(c);
+  unsigned long long* dst = reinterpret_cast<unsigned long long*>(&v);
+#pragma unroll
+  for (int i = 0; i < (int)(sizeof(Ctl) / 8); ++i) dst[i] = __ldcg(src + i);
+  return v;
+}
+
 // engine.hpp:292-307 + the fused CFL cache for the next step, given the
-// step's reduced partials p and outcome (status, index, err_h); thread 0 only
+// step's reduced partials p and outcome (status, index, err_h).  One thread;
+// works on a register copy of the control block (one batch of loads).
 __device__ void finalize_step(const Dev& d, const Part& p, int status, int index, double err_h,
                               cudaGraphConditionalHandle cond, int use_cond) {
-  Ctl* c = d.ctl;
-  const StepParams* sp = d.sp;
-  bool last;
-  const double dt = step_dt(c, sp->t_end, &last);
+  Ctl c = load_ctl(d.ctl);
+  const StepParams sp = *d.sp;
+  const bool last = c.t + c.dts >= sp.t_end;  // engine.hpp:236-237
+  const double dt = last ? sp.t_end - c.t : c.dts;
   if (status != SWE_OK) {  // engine.hpp:168-169, :292-297; state is not committed
-    c->status = status;
-    c->err_index = index;
+    c.status = status;
+    c.err_index = index;
     if (status == SWE_BLOWUP) {
-      c->err_step = c->step;
-      c->err_dt = dt;
-      c->err_h = err_h;
+      c.err_step = c.step;
+      c.err_dt = dt;
+      c.err_h = err_h;
     }
-    c->bad_edge = kNone;
-    c->bad_cell = kNone;
-    c->bad_speed = kNone;
-    c->active = 0;
+    c.bad_edge = kNone;
+    c.bad_cell = kNone;
+    c.bad_speed = kNone;
+    c.active = 0;
+    *d.ctl = c;
     if (use_cond) cudaGraphSetConditional(cond, 0);
     return;
   }
   // commit (engine.hpp:300-307)
-  const double max_speed_pre = c->max_speed;
-  c->clipped += p.clip;
-  c->events += p.events;
-  c->cur ^= 1;
-  c->t = last ? sp->t_end : c->t + dt;
-  c->step += 1;
-  const long long slot = sp->ring ? (c->n_rec % sp->rec_cap) : c->n_rec;
-  if (slot < sp->rec_cap) {
+  const double max_speed_pre = c.max_speed;
+  c.clipped += p.clip;
+  c.events += p.events;
+  c.cur ^= 1;
+  c.t = last ? sp.t_end : c.t + dt;
+  c.step += 1;
+  const long long slot = sp.ring ? (c.n_rec % sp.rec_cap) : c.n_rec;
+  if (slot < sp.rec_cap) {
     swe_step_record r;
-    r.step = c->step;
-    r.t = c->t;
+    r.step = c.step;
+    r.t = c.t;
     r.dt = dt;
     r.max_speed = max_speed_pre;
     r.mass = p.mass;
     d.rec[slot] = r;
   }
-  c->n_rec += 1;
-  set_cfl_cache(c, p, d.P);
+  c.n_rec += 1;
+  set_cfl_cache(&c, p, d.P);
   // continue? (engine.hpp:355-358, :374-375)
-  int go = c->t < sp->t_end && c->step < sp->max_steps && !(c->t >= sp->next_snap - 1e-12) &&
-           (sp->ring || c->n_rec < sp->rec_cap);
-  if (go && c->cfl_bad != kNone) {
-    c->status = SWE_NONFINITE_SPEED;
-    c->err_index = c->cfl_bad;
+  int go = c.t < sp.t_end && c.step < sp.max_steps && !(c.t >= sp.next_snap - 1e-12) &&
+           (sp.ring || c.n_rec < sp.rec_cap);
+  if (go && c.cfl_bad != kNone) {
+    c.status = SWE_NONFINITE_SPEED;
+    c.err_index = c.cfl_bad;
     go = 0;
   }
-  c->active = go;
+  c.active = go;
+  *d.ctl = c;
   if (use_cond) cudaGraphSetConditional(cond, go);
 }
 
-// finalize of a single-domain step; n = number of partials the step kernel wrote
-__global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
-                                                     int use_cond) {
-  Ctl* c = d.ctl;
-  if (!c->active) {
-    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
-    return;
-  }
-  const Part p = reduce_parts(d, n);
-  if (threadIdx.x != 0) return;
+// single-domain step outcome from the reduced partials p (thread 0)
+__device__ void finalize_local(const Dev& d, const Part& p, cudaGraphConditionalHandle cond,
+                               int use_cond) {
+  const Ctl c = load_ctl(d.ctl);
   int status = SWE_OK, index = kNone;
   double err_h = 0.0;
-  if (c->bad_edge != kNone) {  // engine.hpp:168-169
+  if (c.bad_edge != kNone) {  // engine.hpp:168-169
     status = SWE_NEGATIVE_DEPTH;
-    index = c->bad_edge;
-  } else if (c->bad_cell != kNone) {  // engine.hpp:292-297
+    index = c.bad_edge;
+  } else if (c.bad_cell != kNone) {  // engine.hpp:292-297
     status = SWE_BLOWUP;
-    index = c->bad_cell;
-    err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
+    index = c.bad_cell;
+    err_h = d.h[c.cur ^ 1][d.c_new[c.bad_cell]];
   }
   finalize_step(d, p, status, index, err_h, cond, use_cond);
 }
 
 // ---- linked contexts: post / wait (see Link) ------------------------------
+// Executed by one full warp: lane q serves ranks q, q+32, ...
 // kind 0: a step's outcome (partials of the step kernel, error slots);
-// kind 1: the CFL bound of the current state (partials of k_cfl)
-__global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
-  Ctl* c = d.ctl;
-  if (kind == 0 && !c->active) return;
-  const Part p = reduce_parts(d, n);
-  if (threadIdx.x != 0) return;
+// kind 1: the CFL bound of the current state (partials of k_cfl).
+__device__ void post_outcome(const Dev& d, const Part& p, int kind) {
+  const int lane = threadIdx.x & 31;
+  const Ctl c = load_ctl(d.ctl);
   const Link& L = d.L;
   XPost x;
   x.lo = p.lo;
@@ -388,63 +422,97 @@ __global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
   x.index = kNone;
   x.err_h = 0.0;
   x.pad = 0;
-  if (kind == 0 && c->bad_edge != kNone) {
+  if (kind == 0 && c.bad_edge != kNone) {
     x.status = SWE_NEGATIVE_DEPTH;
-    x.index = L.gedge[c->bad_edge];
-  } else if (kind == 0 && c->bad_cell != kNone) {
+    x.index = L.gedge[c.bad_edge];
+  } else if (kind == 0 && c.bad_cell != kNone) {
     x.status = SWE_BLOWUP;
-    x.index = L.gcell[c->bad_cell];
-    x.err_h = d.h[c->cur ^ 1][d.c_new[c->bad_cell]];
+    x.index = L.gcell[c.bad_cell];
+    x.err_h = d.h[c.cur ^ 1][d.c_new[c.bad_cell]];
   }
-  x.bad_speed = c->bad_speed == kNone ? kNone : L.gcell[c->bad_speed];
-  c->bad_edge = kNone;
-  c->bad_cell = kNone;
-  c->bad_speed = kNone;
-  const unsigned long long tag = ++c->xseq;
+  x.bad_speed = c.bad_speed == kNone ? kNone : L.gcell[c.bad_speed];
+  const unsigned long long tag = c.xseq + 1;
   x.tag = tag;
-  for (int q = 0; q < L.nranks; ++q) L.box[q]->slot[tag & 1][L.rank] = x;
-  __threadfence_system();
-  for (int q = 0; q < L.nranks; ++q) st_release_sys(&L.box[q]->flag[L.rank], tag);
+  __syncwarp();
+  if (lane == 0) {
+    d.ctl->bad_edge = kNone;
+    d.ctl->bad_cell = kNone;
+    d.ctl->bad_speed = kNone;
+    d.ctl->xseq = tag;
+  }
+  for (int q = lane; q < L.nranks; q += 32) {
+    L.box[q]->slot[tag & 1][L.rank] = x;
+    __threadfence_system();
+    st_release_sys(&L.box[q]->flag[L.rank], tag);
+  }
+  __syncwarp();
 }
 
-__global__ void k_wait(Dev d, int kind, cudaGraphConditionalHandle cond, int use_cond) {
-  Ctl* c = d.ctl;
-  if (kind == 0 && !c->active) {
-    if (use_cond) cudaGraphSetConditional(cond, 0);
-    return;
-  }
+// wait for every rank's post, combine in rank order, commit (one warp)
+__device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHandle cond,
+                                int use_cond) {
+  const int lane = threadIdx.x & 31;
   const Link& L = d.L;
-  const unsigned long long tag = c->xseq;
+  const unsigned long long tag = __ldcg(&d.ctl->xseq);
   Mailbox* m = L.mine;
   const unsigned long long t0 = global_ns();
   bool timeout = false;
-  for (int q = 0; q < L.nranks && !timeout; ++q)
+  for (int q = lane; q < L.nranks && !timeout; q += 32)
     while (ld_acquire_sys(&m->flag[q]) < tag) {
       if (global_ns() - t0 > L.timeout_ns) {
         timeout = true;
         break;
       }
-      __nanosleep(100);
+      __nanosleep(64);
     }
   // combine in rank order: every rank forms the same sums
   Part g{INFINITY, 0.0, 0.0, 0.0, 0, 0};
   int neg = kNone, blow = kNone, bad = kNone;
   double err_h = 0.0;
-  for (int q = 0; q < L.nranks && !timeout; ++q) {
-    const volatile XPost* s = &m->slot[tag & 1][q];
-    if (s->tag != tag) timeout = true;  // a post from a different exchange
-    g.lo = sel_min(g.lo, s->lo);
-    g.hi = sel_max(g.hi, s->hi);
-    g.mass += s->mass;
-    g.clip += s->clip;
-    g.events += s->events;
-    if (s->status == SWE_NEGATIVE_DEPTH) neg = min(neg, s->index);
-    if (s->status == SWE_BLOWUP && s->index < blow) {
-      blow = s->index;
-      err_h = s->err_h;
+  for (int base = 0; base < L.nranks; base += 32) {
+    const int q = base + lane;
+    XPost s{};
+    if (q < L.nranks && !timeout) {
+      const volatile XPost* v = &m->slot[tag & 1][q];
+      s.lo = v->lo;
+      s.hi = v->hi;
+      s.mass = v->mass;
+      s.clip = v->clip;
+      s.events = v->events;
+      s.tag = v->tag;
+      s.status = v->status;
+      s.index = v->index;
+      s.bad_speed = v->bad_speed;
+      s.err_h = v->err_h;
+      if (s.tag != tag) timeout = true;  // a post from a different exchange
     }
-    bad = min(bad, s->bad_speed);
+    const int cnt = min(32, L.nranks - base);
+    for (int j = 0; j < cnt; ++j) {  // fold lane j's post (rank base + j)
+      const double lo = __shfl_sync(0xffffffffu, s.lo, j);
+      const double hi = __shfl_sync(0xffffffffu, s.hi, j);
+      const double ms = __shfl_sync(0xffffffffu, s.mass, j);
+      const double cl = __shfl_sync(0xffffffffu, s.clip, j);
+      const long long ev = __shfl_sync(0xffffffffu, s.events, j);
+      const int st = __shfl_sync(0xffffffffu, s.status, j);
+      const int ix = __shfl_sync(0xffffffffu, s.index, j);
+      const int bs = __shfl_sync(0xffffffffu, s.bad_speed, j);
+      const double eh = __shfl_sync(0xffffffffu, s.err_h, j);
+      g.lo = sel_min(g.lo, lo);
+      g.hi = sel_max(g.hi, hi);
+      g.mass += ms;
+      g.clip += cl;
+      g.events += ev;
+      if (st == SWE_NEGATIVE_DEPTH) neg = min(neg, ix);
+      if (st == SWE_BLOWUP && ix < blow) {
+        blow = ix;
+        err_h = eh;
+      }
+      bad = min(bad, bs);
+    }
   }
+  timeout = __any_sync(0xffffffffu, timeout);
+  if (lane != 0) return;
+  Ctl* c = d.ctl;
   if (timeout) {
     c->link_err = 1;
     c->status = SWE_NCCL;
@@ -456,11 +524,51 @@ __global__ void k_wait(Dev d, int kind, cudaGraphConditionalHandle cond, int use
   }
   c->bad_speed = bad;
   if (kind == 1) {
-    set_cfl_cache(c, g, d.P);
+    Ctl v = load_ctl(c);
+    set_cfl_cache(&v, g, d.P);
+    *c = v;
     return;
   }
   const int status = neg != kNone ? SWE_NEGATIVE_DEPTH : (blow != kNone ? SWE_BLOWUP : SWE_OK);
   finalize_step(d, g, status, status == SWE_NEGATIVE_DEPTH ? neg : blow, err_h, cond, use_cond);
+}
+
+// kernel forms
+__global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
+                                                     int use_cond) {
+  if (!d.ctl->active) {
+    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x == 0) finalize_local(d, p, cond, use_cond);
+}
+
+__global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
+  if (kind == 0 && !d.ctl->active) return;
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x < 32) post_outcome(d, p, kind);
+}
+
+// post + wait in one launch (the graph / plain path of a linked context)
+__global__ void __launch_bounds__(kBlock) k_exchange(Dev d, int n, int kind,
+                                                     cudaGraphConditionalHandle cond, int use_cond) {
+  if (kind == 0 && !d.ctl->active) {
+    if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  const Part p = reduce_parts(d, n);
+  if (threadIdx.x >= 32) return;
+  post_outcome(d, p, kind);
+  wait_and_commit(d, kind, cond, use_cond);
+}
+
+__global__ void k_wait(Dev d, int kind, cudaGraphConditionalHandle cond, int use_cond) {
+  if (kind == 0 && !d.ctl->active) {
+    if (use_cond) cudaGraphSetConditional(cond, 0);
+    return;
+  }
+  wait_and_commit(d, kind, cond, use_cond);
 }
 
 }  // namespace swe_b200

@@ -120,15 +120,18 @@ const void* tile_kernel(int threads, bool link) {
   return link ? (const void*)k_tile<256, true> : (const void*)k_tile<256, false>;
 }
 
-int launch_update(swe_dev_ctx* x) {  // the step kernel(s) before finalize
+// the step kernel(s) before finalize
+int launch_update(swe_dev_ctx* x) {
   if (x->fused) {
     const bool L = x->linked;
+    const int g = x->grid_tile;
+    const size_t sm = x->tile_smem;
     if (x->tile_threads == 128) {
-      if (L) k_tile<128, true><<<x->grid_tile, 128, x->tile_smem, x->stream>>>(x->d);
-      else k_tile<128, false><<<x->grid_tile, 128, x->tile_smem, x->stream>>>(x->d);
+      if (L) k_tile<128, true><<<g, 128, sm, x->stream>>>(x->d);
+      else k_tile<128, false><<<g, 128, sm, x->stream>>>(x->d);
     } else {
-      if (L) k_tile<256, true><<<x->grid_tile, 256, x->tile_smem, x->stream>>>(x->d);
-      else k_tile<256, false><<<x->grid_tile, 256, x->tile_smem, x->stream>>>(x->d);
+      if (L) k_tile<256, true><<<g, 256, sm, x->stream>>>(x->d);
+      else k_tile<256, false><<<g, 256, sm, x->stream>>>(x->d);
     }
     ++g_launches;
     return cuda_ok(cudaGetLastError(), "k_tile") ? SWE_OK : SWE_CUDA;
@@ -151,16 +154,19 @@ int launch_post(swe_dev_ctx* x, int n, int kind) {
 }
 
 int launch_wait(swe_dev_ctx* x, int kind, cudaGraphConditionalHandle h, int use_cond) {
-  k_wait<<<1, 1, 0, x->stream>>>(x->d, kind, h, use_cond);
+  k_wait<<<1, 32, 0, x->stream>>>(x->d, kind, h, use_cond);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_wait") ? SWE_OK : SWE_CUDA;
 }
 
+int launch_exchange(swe_dev_ctx* x, int n, int kind, cudaGraphConditionalHandle h, int use_cond) {
+  k_exchange<<<1, kBlock, 0, x->stream>>>(x->d, n, kind, h, use_cond);
+  ++g_launches;
+  return cuda_ok(cudaGetLastError(), "k_exchange") ? SWE_OK : SWE_CUDA;
+}
+
 int launch_finalize(swe_dev_ctx* x, cudaGraphConditionalHandle h, int use_cond) {
-  if (x->linked) {
-    if (int rc = launch_post(x, x->n_step_parts(), 0)) return rc;
-    return launch_wait(x, 0, h, use_cond);
-  }
+  if (x->linked) return launch_exchange(x, x->n_step_parts(), 0, h, use_cond);
   k_finalize<<<1, kBlock, 0, x->stream>>>(x->d, x->n_step_parts(), h, use_cond);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_finalize") ? SWE_OK : SWE_CUDA;
@@ -184,10 +190,8 @@ int ensure_cfl(swe_dev_ctx* x, bool force = false) {
   if (x->h_ctl->cfl_valid && !force) return SWE_OK;
   k_cfl<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
   ++g_launches;
-  if (x->linked) {  // the global bound: every rank posts, then waits
-    if (int rc = launch_post(x, x->grid_cell, 1)) return rc;
-    return launch_wait(x, 1, cudaGraphConditionalHandle{}, 0);
-  }
+  if (x->linked)  // the global bound: every rank posts, then waits
+    return launch_exchange(x, x->grid_cell, 1, cudaGraphConditionalHandle{}, 0);
   k_prepare<<<1, kBlock, 0, x->stream>>>(x->d, x->grid_cell);
   ++g_launches;
   CK(cudaGetLastError());
@@ -491,9 +495,26 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.E = E;
   d.C_own = (m->n_owned > 0 && m->n_owned <= C) ? m->n_owned : C;
   d.P = Phys{params->g, params->h_dry, params->cfl, params->dt_max, params->h_ref};
-  int T = 256;
-  if (const char* env = std::getenv("SWE_TILE_CELLS")) T = std::max(32, std::atoi(env));
   if (const char* env = std::getenv("SWE_TILE_THREADS")) x->tile_threads = std::atoi(env) == 128 ? 128 : 256;
+  // tile size: at most 256 cells (measured best, r02), shrunk so the tiles
+  // fill whole waves of the persistent grid (a 1.28M-cell part has 4.2 waves
+  // of 256-cell tiles: the last one 23% busy)
+  int T = 256;
+  if (const char* env = std::getenv("SWE_TILE_CELLS")) {
+    T = std::max(32, std::atoi(env));
+  } else {
+    int sms = 148, occ = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaFuncSetAttribute(tile_kernel(x->tile_threads, false),
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tile_smem_bytes(256, 0));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel(x->tile_threads, false),
+                                                  x->tile_threads, tile_smem_bytes(256, 0));
+    const long long grid = (long long)sms * std::max(1, occ);
+    const long long waves = std::max(1LL, (d.C_own + 256 * grid - 1) / (256 * grid));
+    const long long t = (d.C_own + waves * grid - 1) / (waves * grid);
+    T = (int)std::min(256LL, std::max(32LL, (t + 7) / 8 * 8));
+    cudaGetLastError();
+  }
   d.T = T;
   d.ntiles = (d.C_own + T - 1) / T;
 

@@ -256,11 +256,13 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%, r02).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
-  return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;
+  return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
 }
 
 // LINK: linked context -- after the update, push the tile's cells that peers
-// hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh)
+// hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
+// (Finalizing in the kernel's last block instead of a separate launch was
+// measured slower, r02: its register copies spill into the main loop.)
 template <int NT, bool LINK>
 __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   extern __shared__ double smem[];
@@ -296,6 +298,11 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     }
     const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
     const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
+    int p0 = 0, p1 = 0;  // push-list range of the tile (linked)
+    if (LINK) {
+      p0 = __ldg(d.L.tile_push + t);
+      p1 = __ldg(d.L.tile_push + t + 1);
+    }
     __syncthreads();
 
     // owned + halo edges -> contributions of the in-tile sides
@@ -353,15 +360,14 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
         ay += ty[3 * i + k];
       }
       const Cons u = cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
-      if (LINK) {  // the tile's new state, for the push below
+      if (LINK && p1 > p0) {  // the tile's new state, for the push below
         sh[i] = u.h;
         sq[i] = u.qx;
         sr[i] = u.qy;
       }
     }
     __syncthreads();
-    if (LINK) {
-      const int p0 = __ldg(d.L.tile_push + t), p1 = __ldg(d.L.tile_push + t + 1);
+    if (LINK && p1 > p0) {
       for (int j = p0 + threadIdx.x; j < p1; j += NT) {
         const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);
         double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + j) + 3 * (cur ^ 1);
@@ -369,7 +375,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
         dst[1][g] = sq[i];
         dst[2][g] = sr[i];
       }
-      if (p1 > p0) __threadfence_system();
+      __threadfence_system();
       __syncthreads();
     }
   }
