@@ -133,6 +133,12 @@ SWE_API int swe_dev_advance(swe_dev_ctx* ctx, double t_end, long long max_steps,
  * bench.hpp:91-110), asynchronous on the context stream: no host sync, no
  * record download.  Status is checked by the next synchronous call. */
 SWE_API int swe_dev_advance_n_async(swe_dev_ctx* ctx, long long n, double t_end);
+/* swe_dev_advance split in two: enqueue the graph launch (no host sync when
+ * the CFL cache is known valid), then collect status + records. */
+SWE_API int swe_dev_advance_async(swe_dev_ctx* ctx, double t_end, long long max_steps,
+                                  double next_snapshot, long long max_records);
+SWE_API int swe_dev_records(swe_dev_ctx* ctx, swe_step_record* series, long long max_records,
+                            long long* n_done, swe_status* st);
 SWE_API int swe_dev_synchronize(swe_dev_ctx* ctx, swe_status* st);
 
 /* compute_fluxes (engine.hpp:138-170) on the current state; left/right are

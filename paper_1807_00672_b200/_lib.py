@@ -65,6 +65,8 @@ _SIGS = {
     "swe_dev_advance": (c_int, [c_void_p, c_double, c_ll, c_double, c_void_p, c_ll, P_ll,
                                 C.POINTER(swe_status)]),
     "swe_dev_advance_n_async": (c_int, [c_void_p, c_ll, c_double]),
+    "swe_dev_advance_async": (c_int, [c_void_p, c_double, c_ll, c_double, c_ll]),
+    "swe_dev_records": (c_int, [c_void_p, c_void_p, c_ll, P_ll, C.POINTER(swe_status)]),
     "swe_dev_synchronize": (c_int, [c_void_p, C.POINTER(swe_status)]),
     "swe_dev_compute_fluxes": (c_int, [c_void_p, c_void_p, c_void_p, C.POINTER(swe_status)]),
     "swe_dev_total_mass": (c_int, [c_void_p, P_double]),

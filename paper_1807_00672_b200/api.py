@@ -481,6 +481,22 @@ class DeviceSolver:
         _status(rc, st, "swe_dev_advance")
         return out
 
+    def advance_async(self, t_end: float, max_steps: int = 2**62,
+                      next_snapshot: float = float("inf"), max_records: int = 1 << 16):
+        """Enqueue the graph-launched advance; collect with records()."""
+        _check(self.lib.swe_dev_advance_async(self.ctx, t_end, max_steps, next_snapshot,
+                                              max_records), "swe_dev_advance_async")
+
+    def records(self, max_records: int = 1 << 16) -> np.ndarray:
+        recs = (L.swe_step_record * max_records)()
+        n, st = C.c_longlong(), L.swe_status()
+        rc = self.lib.swe_dev_records(self.ctx, recs, max_records, C.byref(n), C.byref(st))
+        out = np.array([(r.step, r.t, r.dt, r.max_speed, r.mass)
+                        for r in recs[:min(n.value, max_records)]],
+                       dtype=np.float64).reshape(-1, 5)
+        _status(rc, st, "swe_dev_records")
+        return out
+
     def advance_n_async(self, n: int, t_end: float = float("inf")):
         _check(self.lib.swe_dev_advance_n_async(self.ctx, n, t_end), "swe_dev_advance_n_async")
 

@@ -292,6 +292,8 @@ __global__ void __launch_bounds__(kBlock) k_prepare(Dev d, int n) {
   if (threadIdx.x == 0) set_cfl_cache(d.ctl, p, d.P);
 }
 
+__global__ void k_set_params(StepParams* sp, StepParams v) { *sp = v; }
+
 // gate: opens a launch sequence (run() loop entry, engine.hpp:355-358)
 __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   Ctl* c = d.ctl;

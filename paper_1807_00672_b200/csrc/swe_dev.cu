@@ -73,7 +73,6 @@ struct swe_dev_ctx {
   Ctl* ctl = nullptr;          // device
   StepParams* sp = nullptr;    // device
   Ctl* h_ctl = nullptr;        // pinned host mirror
-  StepParams* h_sp = nullptr;  // pinned host
   swe_step_record* rec = nullptr;
   long long rec_cap = 0;
   double *stage_h = nullptr, *stage_qx = nullptr, *stage_qy = nullptr;
@@ -89,6 +88,7 @@ struct swe_dev_ctx {
   size_t arena_bytes = 0;
   bool linked = false;
   bool cfl_posted = false;  // link_phase: a CFL exchange awaits its wait
+  bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
   // graph
@@ -185,11 +185,18 @@ int sync_ctl(swe_dev_ctx* x) {
 }
 
 // CFL cache of the current state if stale (after set_state)
+// (no host sync when the host already knows the cache is valid: the step
+// kernels keep it valid; set_state / link invalidate it)
 int ensure_cfl(swe_dev_ctx* x, bool force = false) {
+  if (x->cfl_host_valid && !force) return SWE_OK;
   if (int rc = sync_ctl(x)) return rc;
-  if (x->h_ctl->cfl_valid && !force) return SWE_OK;
+  if (x->h_ctl->cfl_valid && !force) {
+    x->cfl_host_valid = true;
+    return SWE_OK;
+  }
   k_cfl<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
   ++g_launches;
+  x->cfl_host_valid = true;
   if (x->linked)  // the global bound: every rank posts, then waits
     return launch_exchange(x, x->grid_cell, 1, cudaGraphConditionalHandle{}, 0);
   k_prepare<<<1, kBlock, 0, x->stream>>>(x->d, x->grid_cell);
@@ -198,15 +205,20 @@ int ensure_cfl(swe_dev_ctx* x, bool force = false) {
   return SWE_OK;
 }
 
+// step parameters travel as a kernel argument (captured at launch: no
+// host buffer to race with when launches are only enqueued)
 int write_params(swe_dev_ctx* x, double t_end, long long max_steps, double next_snap,
                  long long rec_cap, int ring, int mode = 0) {
-  x->h_sp->t_end = t_end;
-  x->h_sp->max_steps = max_steps;
-  x->h_sp->next_snap = next_snap;
-  x->h_sp->rec_cap = rec_cap;
-  x->h_sp->ring = ring;
-  x->h_sp->mode = mode;
-  CK(cudaMemcpyAsync(x->sp, x->h_sp, sizeof(StepParams), cudaMemcpyHostToDevice, x->stream));
+  StepParams v;
+  v.t_end = t_end;
+  v.max_steps = max_steps;
+  v.next_snap = next_snap;
+  v.rec_cap = rec_cap;
+  v.ring = ring;
+  v.mode = mode;
+  k_set_params<<<1, 1, 0, x->stream>>>(x->sp, v);
+  ++g_launches;
+  CK(cudaGetLastError());
   return SWE_OK;
 }
 
@@ -576,7 +588,6 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     return bail(SWE_CUDA);
   }
   if (!cuda_ok(cudaMallocHost(&x->h_ctl, sizeof(Ctl)), "cudaMallocHost")) return bail(SWE_CUDA);
-  if (!cuda_ok(cudaMallocHost(&x->h_sp, sizeof(StepParams)), "cudaMallocHost")) return bail(SWE_CUDA);
   d.ctl = x->ctl;
   d.sp = x->sp;
   d.rec = x->rec;
@@ -643,7 +654,6 @@ int swe_dev_destroy(swe_dev_ctx* x) {
   cudaFree(x->halo_send);
   cudaFree(x->halo_recv);
   if (x->h_ctl) cudaFreeHost(x->h_ctl);
-  if (x->h_sp) cudaFreeHost(x->h_sp);
   if (x->stream) cudaStreamDestroy(x->stream);
   delete x;
   return SWE_OK;
@@ -672,6 +682,7 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
   c.active = 0;
   c.bad_edge = c.bad_cell = c.bad_speed = kNone;
   c.link_err = 0;
+  x->cfl_host_valid = false;
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -802,6 +813,30 @@ int swe_dev_advance(swe_dev_ctx* x, double t_end, long long max_steps, double ne
   if (series && n > 0)
     CK(cudaMemcpy(series, x->rec, sizeof(swe_step_record) * (size_t)std::min(n, cap),
                   cudaMemcpyDeviceToHost));
+  return code;
+}
+
+int swe_dev_advance_async(swe_dev_ctx* x, double t_end, long long max_steps, double next_snap,
+                          long long max_records) {
+  if (!x) return fail_invalid("null context");
+  if (!x->exec) return fail_invalid("swe_dev_advance_async: context was created without a graph");
+  const long long cap = std::min<long long>(max_records > 0 ? max_records : x->rec_cap, x->rec_cap);
+  if (int rc = ensure_cfl(x)) return rc;
+  if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
+  CK(cudaGraphLaunch(x->exec, x->stream));
+  ++g_launches;
+  return SWE_OK;
+}
+
+int swe_dev_records(swe_dev_ctx* x, swe_step_record* series, long long max_records,
+                    long long* n_done, swe_status* st) {
+  if (!x) return fail_invalid("null context");
+  const int code = read_status(x, st);
+  const long long n = x->h_ctl->n_rec;
+  if (n_done) *n_done = n;
+  const long long m = std::min(n, std::min<long long>(max_records, x->rec_cap));
+  if (series && m > 0)
+    CK(cudaMemcpy(series, x->rec, sizeof(swe_step_record) * (size_t)m, cudaMemcpyDeviceToHost));
   return code;
 }
 
@@ -1128,6 +1163,7 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
   // the CFL cache must be re-formed globally; the graph gains the exchange
   if (int rc = sync_ctl(x)) return rc;
   x->h_ctl->cfl_valid = 0;
+  x->cfl_host_valid = false;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, x->stream));
   if (x->exec) {
     CK(cudaGraphExecDestroy(x->exec));

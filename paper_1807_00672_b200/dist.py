@@ -399,6 +399,23 @@ class LinkedPart:
     def advance_async(self, n: int, t_end=float("inf")):
         _check(self.lib.swe_dev_advance_n_async(self.ctx, n, t_end), "advance_n_async")
 
+    def launch(self, t_end=1e30, max_steps=1 << 62, next_snapshot=float("inf"),
+               max_records=1 << 16):
+        """advance() split: enqueue the graph launch only (collective)."""
+        _check(self.lib.swe_dev_advance_async(self.ctx, t_end, max_steps, next_snapshot,
+                                              max_records), "swe_dev_advance_async")
+
+    def records(self, max_records=1 << 16):
+        recs = (L.swe_step_record * max_records)()
+        n, st = C.c_longlong(), L.swe_status()
+        rc = self.lib.swe_dev_records(self.ctx, recs, max_records, C.byref(n), C.byref(st))
+        out = np.array([(r.step, r.t, r.dt, r.max_speed, r.mass)
+                        for r in recs[:min(n.value, max_records)]],
+                       dtype=np.float64).reshape(-1, 5)
+        if rc:
+            self.raise_status(rc, st)
+        return out
+
     def synchronize(self):
         st = L.swe_status()
         rc = self.lib.swe_dev_synchronize(self.ctx, C.byref(st))

@@ -351,3 +351,21 @@ def test_cpp_drop_in_driver(golden):
     assert out["nan_msg"] == "stable_dt: non-finite velocity in cell 5"
     assert out["neg_msg"].startswith("compute_fluxes: negative depth at edge ")
     assert out["cfg_msg"] == "run: t_end must be > 0"
+
+
+def test_advance_async_equals_advance():
+    """swe_dev_advance_async + swe_dev_records == swe_dev_advance."""
+    sc = api.make_scenario("three_mounds_friction", scale=0.05)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    a, b = api.DeviceSolver(m), api.DeviceSolver(m)
+    a.set_state(sc.state)
+    b.set_state(sc.state)
+    ra = a.advance(1e30, max_steps=120)
+    b.advance_async(1e30, max_steps=60)
+    b.advance_async(1e30, max_steps=120)  # two launches queued back to back
+    rb = b.records()
+    assert len(rb) == 60 and bit_equal(rb, ra[60:])
+    sa, _, _ = a.get_state()
+    sb, _, _ = b.get_state()
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(sa, k), getattr(sb, k)), k
