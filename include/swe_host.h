@@ -75,6 +75,20 @@ SWE_API void swe_host_local_plan(void* local, int* peers, int* send_counts, int*
                                  int* send_cells, int* recv_cells);
 SWE_API void swe_host_local_free(void* local);
 
+/* SWEMESH 1 mesh files (include/swe/swemesh.hpp; reference io.hpp:80-165):
+ * parallel parse / format, the reference's values and error texts.  A file
+ * handle owns a raw mesh (borrowed by swe_host_swemesh_raw, usable with
+ * swe_host_raw_* and swe_host_build_mesh) + bed + manning.  threads <= 0:
+ * all cores.  NULL / 7 (io error) with the message in err. */
+SWE_API void* swe_host_swemesh_read(const char* path, int threads, char* err, int errlen);
+SWE_API void* swe_host_swemesh_parse(const char* text, long long size, int threads, char* err,
+                                     int errlen);
+SWE_API void* swe_host_swemesh_raw(void* file);
+SWE_API void swe_host_swemesh_fields(void* file, double* bed, double* manning);
+SWE_API void swe_host_swemesh_free(void* file);
+SWE_API int swe_host_swemesh_write(const char* path, void* raw, const double* bed,
+                                   const double* manning, int threads, char* err, int errlen);
+
 #ifdef __cplusplus
 }
 #endif

@@ -398,3 +398,62 @@ class RefMesh:
         return dict(h=h, qx=qx, qy=qy, t=tt.value, step=ss.value,
                     series=series[:min(nr.value, max_rows)].copy(), stats=stats,
                     snaps=snaps[:ns.value].tolist(), rc=rc, error=err.value.decode())
+
+
+REF_IO_SO = HERE / "_ref" / "libswe_ref_io.so"
+
+
+class RefIO:
+    """The reference's SWEMESH reader / writer (io.hpp:80-165) through
+    oracle/_ref/libswe_ref_io.so -- the checker of include/swe/swemesh.hpp."""
+
+    @staticmethod
+    def available() -> bool:
+        return REF_IO_SO.exists()
+
+    def __init__(self):
+        if not REF_IO_SO.exists():
+            raise FileNotFoundError(f"{REF_IO_SO} not built (needs /root/reference at build time)")
+        L = self.lib = C.CDLL(str(REF_IO_SO))
+        L.refio_parse.restype = vp
+        L.refio_parse.argtypes = [C.c_char_p, C.c_longlong, C.c_char_p, ci]
+        L.refio_read.restype = vp
+        L.refio_read.argtypes = [C.c_char_p, C.c_char_p, ci]
+        L.refio_sizes.argtypes = [vp, C.POINTER(ci), C.POINTER(ci)]
+        L.refio_export.argtypes = [vp, vp, vp, vp, vp]
+        L.refio_free.argtypes = [vp]
+        L.refio_write.restype = ci
+        L.refio_write.argtypes = [C.c_char_p, ci, vp, ci, vp, vp, vp, C.c_char_p, ci]
+
+    def _result(self, h, err):
+        if not h:
+            raise ValueError(err.value.decode(errors="replace"))
+        nn, nc = ci(), ci()
+        self.lib.refio_sizes(h, C.byref(nn), C.byref(nc))
+        xy = np.empty((nn.value, 2))
+        tris = np.empty((nc.value, 3), dtype=np.int32)
+        bed, man = np.empty(nc.value), np.empty(nc.value)
+        self.lib.refio_export(h, xy.ctypes.data, tris.ctypes.data, bed.ctypes.data,
+                              man.ctypes.data)
+        self.lib.refio_free(h)
+        return xy, tris, bed, man
+
+    def parse(self, text):
+        """-> (nodes[nn,2], tris[nc,3], bed, manning); ValueError(reference message)."""
+        b = text.encode() if isinstance(text, str) else bytes(text)
+        err = C.create_string_buffer(1024)
+        return self._result(self.lib.refio_parse(b, len(b), err, 1024), err)
+
+    def read(self, path):
+        err = C.create_string_buffer(1024)
+        return self._result(self.lib.refio_read(str(path).encode(), err, 1024), err)
+
+    def write(self, path, nodes, tris, bed, man):
+        nodes = np.ascontiguousarray(nodes, dtype=np.float64)
+        tris = np.ascontiguousarray(tris, dtype=np.int32)
+        bed = np.ascontiguousarray(bed, dtype=np.float64)
+        man = np.ascontiguousarray(man, dtype=np.float64)
+        err = C.create_string_buffer(1024)
+        if self.lib.refio_write(str(path).encode(), len(nodes), nodes.ctypes.data, len(tris),
+                                tris.ctypes.data, bed.ctypes.data, man.ctypes.data, err, 1024):
+            raise ValueError(err.value.decode())

@@ -118,6 +118,13 @@ _SIGS = {
     "swe_host_local_export": (None, [c_void_p] + [c_void_p] * 15),
     "swe_host_local_plan": (None, [c_void_p] + [c_void_p] * 5),
     "swe_host_local_free": (None, [c_void_p]),
+    "swe_host_swemesh_read": (c_void_p, [c_char_p, c_int, c_char_p, c_int]),
+    "swe_host_swemesh_parse": (c_void_p, [c_char_p, c_ll, c_int, c_char_p, c_int]),
+    "swe_host_swemesh_raw": (c_void_p, [c_void_p]),
+    "swe_host_swemesh_fields": (None, [c_void_p, c_void_p, c_void_p]),
+    "swe_host_swemesh_free": (None, [c_void_p]),
+    "swe_host_swemesh_write": (c_int, [c_char_p, c_void_p, c_void_p, c_void_p, c_int, c_char_p,
+                                       c_int]),
     # the C++ drop-in engine behind reference-shaped entry points
     "swe_api_compute_fluxes": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p,
                                        c_void_p, c_void_p, c_int, c_char_p, c_int]),

@@ -48,7 +48,12 @@ class DeviceError(SweError):
     """CUDA runtime failure (no reference counterpart)"""
 
 
-_KINDS = {1: NumericError, 2: ConfigError, 3: MeshError, 4: CaseError, 5: DeviceError}
+class IoError(SweError):
+    """swe::io_error"""
+
+
+_KINDS = {1: NumericError, 2: ConfigError, 3: MeshError, 4: CaseError, 5: DeviceError,
+          7: IoError}
 
 
 def _raise(kind: int, msg: bytes | str):
@@ -98,7 +103,8 @@ class FieldState:
 class RawMesh:
     """swe::RawMesh (mesh.hpp:14-17); owns a host handle."""
 
-    def __init__(self, handle):
+    def __init__(self, handle, owner=None):
+        """owner: object that owns a borrowed handle (kept alive), else we own it."""
         if not handle:
             raise MeshError("null raw mesh")
         self._lib = L.load()
@@ -108,7 +114,8 @@ class RawMesh:
         self.nodes = np.empty((nn.value, 2))
         self.triangles = np.empty((nc.value, 3), dtype=np.int32)
         self._lib.swe_host_raw_export(handle, L.ptr(self.nodes), L.ptr(self.triangles))
-        self._owned = True
+        self._owner = owner
+        self._owned = owner is None
 
     def __del__(self):
         if getattr(self, "_owned", False) and self.handle:
@@ -125,6 +132,56 @@ class RawMesh:
     @property
     def n_cells(self):
         return len(self.triangles)
+
+
+class _SweMeshFile:
+    """owns a swe_host_swemesh_* handle"""
+
+    def __init__(self, h):
+        self._lib, self.h = L.load(), h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self._lib.swe_host_swemesh_free(self.h)
+            self.h = None
+
+
+def _swemesh_result(h, err):
+    if not h:
+        _raise(7, err.value)
+    f = _SweMeshFile(h)
+    raw = RawMesh(f._lib.swe_host_swemesh_raw(h), owner=f)
+    bed, man = np.empty(raw.n_cells), np.empty(raw.n_cells)
+    f._lib.swe_host_swemesh_fields(h, L.ptr(bed), L.ptr(man))
+    return raw, bed, man
+
+
+def read_swemesh(path, threads: int = 0):
+    """SWEMESH 1 file -> (RawMesh, bed, manning) (io.hpp read_mesh_native_file,
+    parsed in parallel by include/swe/swemesh.hpp); raises IoError."""
+    err = _errbuf()
+    return _swemesh_result(L.load().swe_host_swemesh_read(str(path).encode(), threads, err,
+                                                          len(err)), err)
+
+
+def parse_swemesh(text, threads: int = 0):
+    """SWEMESH 1 text (str or bytes) -> (RawMesh, bed, manning)."""
+    b = text.encode() if isinstance(text, str) else bytes(text)
+    err = _errbuf()
+    return _swemesh_result(L.load().swe_host_swemesh_parse(b, len(b), threads, err, len(err)), err)
+
+
+def write_swemesh(path, raw: RawMesh, bed, manning, threads: int = 0):
+    """io.hpp write_mesh_native_file (17 significant digits), formatted in parallel."""
+    bed = np.ascontiguousarray(bed, dtype=np.float64)
+    man = np.ascontiguousarray(manning, dtype=np.float64)
+    if len(bed) != raw.n_cells or len(man) != raw.n_cells:
+        raise IoError("write_mesh_native: bed / manning size != cell count")
+    err = _errbuf()
+    rc = L.load().swe_host_swemesh_write(str(path).encode(), raw.handle, L.ptr(bed), L.ptr(man),
+                                         threads, err, len(err))
+    if rc:
+        _raise(rc, err.value)
 
 
 def generate_square_mesh(nx: int, ny: int, lx: float, ly: float) -> RawMesh:

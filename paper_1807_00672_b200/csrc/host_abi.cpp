@@ -8,6 +8,7 @@
 #include "swe/engine.hpp"
 #include "swe/partition.hpp"
 #include "swe/mesh.hpp"
+#include "swe/swemesh.hpp"
 #include "swe_host.h"
 
 namespace {
@@ -454,3 +455,49 @@ EXPORT void swe_host_local_plan(void* lp, int* peers, int* send_counts, int* rec
 }
 
 EXPORT void swe_host_local_free(void* lp) { delete static_cast<swe::LocalMesh*>(lp); }
+
+// ---- SWEMESH 1 files (swe/swemesh.hpp; reference io.hpp:80-165) ----------
+EXPORT void* swe_host_swemesh_read(const char* path, int threads, char* err, int errlen) {
+  try {
+    return new swe::swemesh::NativeFile(swe::swemesh::read_file(path, threads));
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return nullptr;
+  }
+}
+
+EXPORT void* swe_host_swemesh_parse(const char* text, long long size, int threads, char* err,
+                                    int errlen) {
+  try {
+    return new swe::swemesh::NativeFile(swe::swemesh::parse(text, (size_t)size, threads));
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return nullptr;
+  }
+}
+
+EXPORT void* swe_host_swemesh_raw(void* f) {
+  return &static_cast<swe::swemesh::NativeFile*>(f)->raw;
+}
+
+EXPORT void swe_host_swemesh_fields(void* f, double* bed, double* manning) {
+  const auto& m = *static_cast<swe::swemesh::NativeFile*>(f);
+  if (bed) std::memcpy(bed, m.bed.data(), m.bed.size() * sizeof(double));
+  if (manning) std::memcpy(manning, m.manning.data(), m.manning.size() * sizeof(double));
+}
+
+EXPORT void swe_host_swemesh_free(void* f) { delete static_cast<swe::swemesh::NativeFile*>(f); }
+
+EXPORT int swe_host_swemesh_write(const char* path, void* raw, const double* bed,
+                                  const double* manning, int threads, char* err, int errlen) {
+  try {
+    const auto& r = *static_cast<swe::RawMesh*>(raw);
+    const size_t nc = r.triangles.size();
+    swe::swemesh::write_file(path, r, std::vector<double>(bed, bed + nc),
+                             std::vector<double>(manning, manning + nc), threads);
+    return 0;
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return 7;
+  }
+}
