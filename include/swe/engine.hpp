@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <limits>
@@ -327,16 +328,47 @@ inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
   std::vector<swe_step_record> recs(1 << 16);
   if (static_cast<int>(sim.next.h.size()) != mesh.n_cells()) sim.next.resize(mesh.n_cells());
 
-  while (sim.t < opt.t_end) {
+  // Segments of the loop run on the device (one graph launch each, ending at
+  // t_end, a snapshot time or a full record buffer).  A snapshot is permuted
+  // into a device slot and copied (copy stream) straight into sim.current --
+  // page-locked for the run -- while the NEXT segment already runs;
+  // on_snapshot is called when the copy has landed, so the device does not
+  // wait for the host's I/O.
+  const size_t C = static_cast<size_t>(mesh.n_cells());
+  struct Locked {  // cudaHostRegister of the state vectors for the run
+    std::vector<void*> ps;
+    ~Locked() {
+      for (void* p : ps) swe_dev_host_unregister(p);
+    }
+  } locked;
+  bool async_snapshots = opt.on_snapshot && std::getenv("SWE_SYNC_SNAPSHOTS") == nullptr;
+  if (async_snapshots) {
+    for (double* p : {sim.current.h.data(), sim.current.qx.data(), sim.current.qy.data()}) {
+      if (swe_dev_host_register(p, static_cast<long long>(C * sizeof(double))) != SWE_OK) {
+        async_snapshots = false;  // not lockable: synchronous snapshots
+        break;
+      }
+      locked.ps.push_back(p);
+    }
+  }
+  auto launch = [&] {
+    const double snap = opt.on_snapshot ? next_snapshot : std::numeric_limits<double>::infinity();
+    detail::DeviceMesh::check(swe_dev_advance_async(ctx, opt.t_end, opt.max_steps, snap,
+                                                    static_cast<long long>(recs.size())),
+                              "swe_dev_advance_async");
+  };
+  bool running = sim.t < opt.t_end;
+  if (running) {
     if (sim.step >= opt.max_steps)
       throw numeric_error("run: exceeded max_steps=" + std::to_string(opt.max_steps) +
                           " before reaching t_end (t=" + std::to_string(sim.t) + ")");
-    const double snap = opt.on_snapshot ? next_snapshot : std::numeric_limits<double>::infinity();
+    launch();
+  }
+  while (running) {
     long long n = 0;
     swe_status st{};
     const auto b0 = clock::now();
-    const int rc = swe_dev_advance(ctx, opt.t_end, opt.max_steps, snap, recs.data(),
-                                   static_cast<long long>(recs.size()), &n, &st);
+    const int rc = swe_dev_records(ctx, recs.data(), static_cast<long long>(recs.size()), &n, &st);
     rs.wall_update_s += std::chrono::duration<double>(clock::now() - b0).count();
     for (long long i = 0; i < n; ++i) {
       const swe_step_record& r = recs[static_cast<size_t>(i)];
@@ -362,12 +394,31 @@ inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
       detail::download(dm, sim.current);
       detail::raise(st, nullptr);
     }
-    if (opt.on_snapshot && n > 0 && (sim.t >= opt.t_end || sim.t >= next_snapshot - 1e-12)) {
-      detail::download(dm, sim.current);
-      opt.on_snapshot(sim.current, sim.t, sim.step);
+    bool due = opt.on_snapshot && n > 0 && (sim.t >= opt.t_end || sim.t >= next_snapshot - 1e-12);
+    if (due) {
+      if (!async_snapshots) {
+        detail::download(dm, sim.current);
+        opt.on_snapshot(sim.current, sim.t, sim.step);
+        due = false;
+      } else {
+        detail::DeviceMesh::check(
+            swe_dev_snapshot_async(ctx, 0, sim.current.h.data(), sim.current.qx.data(),
+                                   sim.current.qy.data()),
+            "swe_dev_snapshot_async");
+      }
       if (opt.snapshot_interval > 0.0)
         while (next_snapshot <= sim.t) next_snapshot += opt.snapshot_interval;
     }
+    running = sim.t < opt.t_end;
+    const bool over = running && sim.step >= opt.max_steps;
+    if (running && !over) launch();  // the device steps on while the snapshot lands
+    if (due) {
+      detail::DeviceMesh::check(swe_dev_snapshot_wait(ctx, 0), "swe_dev_snapshot_wait");
+      opt.on_snapshot(sim.current, sim.t, sim.step);
+    }
+    if (over)
+      throw numeric_error("run: exceeded max_steps=" + std::to_string(opt.max_steps) +
+                          " before reaching t_end (t=" + std::to_string(sim.t) + ")");
   }
   detail::download(dm, sim.current);
   long long events = 0;

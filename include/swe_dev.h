@@ -141,6 +141,21 @@ SWE_API int swe_dev_records(swe_dev_ctx* ctx, swe_step_record* series, long long
                             long long* n_done, swe_status* st);
 SWE_API int swe_dev_synchronize(swe_dev_ctx* ctx, swe_status* st);
 
+/* Asynchronous snapshot of the current state (as of this point in the
+ * context's stream) into host arrays h/qx/qy [C] (reference numbering; pinned
+ * memory -- swe_dev_host_alloc -- lets the copy overlap later steps).  Two
+ * slots: a slot's previous copy is waited for before it is reused.
+ * swe_dev_snapshot_wait blocks until the slot's copy has landed. */
+SWE_API int swe_dev_snapshot_async(swe_dev_ctx* ctx, int slot, double* h, double* qx, double* qy);
+SWE_API int swe_dev_snapshot_wait(swe_dev_ctx* ctx, int slot);
+/* Page-locked host memory (cudaMallocHost) for callers without CUDA headers. */
+SWE_API void* swe_dev_host_alloc(long long bytes);
+SWE_API void swe_dev_host_free(void* p);
+/* Page-lock (cudaHostRegister) / release existing host memory, e.g. the
+ * caller's state vectors, so snapshot copies land in them at full speed. */
+SWE_API int swe_dev_host_register(void* p, long long bytes);
+SWE_API int swe_dev_host_unregister(void* p);
+
 /* compute_fluxes (engine.hpp:138-170) on the current state; left/right are
  * [3E] Flux3 arrays in reference numbering. */
 SWE_API int swe_dev_compute_fluxes(swe_dev_ctx* ctx, double* left, double* right, swe_status* st);

@@ -68,6 +68,12 @@ _SIGS = {
     "swe_dev_advance_async": (c_int, [c_void_p, c_double, c_ll, c_double, c_ll]),
     "swe_dev_records": (c_int, [c_void_p, c_void_p, c_ll, P_ll, C.POINTER(swe_status)]),
     "swe_dev_synchronize": (c_int, [c_void_p, C.POINTER(swe_status)]),
+    "swe_dev_snapshot_async": (c_int, [c_void_p, c_int, c_void_p, c_void_p, c_void_p]),
+    "swe_dev_snapshot_wait": (c_int, [c_void_p, c_int]),
+    "swe_dev_host_alloc": (c_void_p, [c_ll]),
+    "swe_dev_host_free": (None, [c_void_p]),
+    "swe_dev_host_register": (c_int, [c_void_p, c_ll]),
+    "swe_dev_host_unregister": (c_int, [c_void_p]),
     "swe_dev_compute_fluxes": (c_int, [c_void_p, c_void_p, c_void_p, C.POINTER(swe_status)]),
     "swe_dev_total_mass": (c_int, [c_void_p, P_double]),
     "swe_dev_set_profiling": (c_int, [c_void_p, c_int]),
@@ -134,7 +140,7 @@ _SIGS = {
                                 P_long, P_long, c_char_p, c_int]),
     "swe_api_run": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, P_double, P_long,
                             c_double, c_double, c_long, c_int, c_void_p, c_long, P_long, c_void_p,
-                            c_void_p, c_long, P_long, c_char_p, c_int]),
+                            c_void_p, c_long, P_long, c_void_p, c_char_p, c_int]),
 }
 
 # every symbol include/swe_dev.h and include/swe_host.h declare

@@ -418,11 +418,16 @@ STAT_KEYS = ("steps", "t_final", "mass_initial", "mass_final", "mass_drift_rel",
 
 def run(mesh: Mesh, state: FieldState, t_end: float, t: float = 0.0, step: int = 0,
         snapshot_interval: float = 0.0, max_steps: int = 100_000_000, max_rows: int = 1 << 20,
-        snapshots: bool = False, params: PhysParams = PhysParams(), device: int = 0) -> RunResult:
-    """swe::run (engine.hpp:335-394); state updated in place."""
+        snapshots: bool = False, params: PhysParams = PhysParams(), device: int = 0,
+        snapshot_fields: int = 0) -> RunResult:
+    """swe::run (engine.hpp:335-394); state updated in place.  snapshot_fields
+    = k > 0 also keeps the first k snapshot states (RunResult.fields [k,3,C])."""
     series = np.zeros((max_rows, 5))
     stats = np.zeros(9)
     snaps = np.zeros(4096)
+    fields = np.zeros((snapshot_fields, 3, mesh.n_cells)) if snapshot_fields else None
+    if snapshot_fields:
+        snaps = np.zeros(snapshot_fields)
     tt, ss = C.c_double(t), C.c_long(step)
     n_rows, n_snaps = C.c_long(), C.c_long()
     err = _errbuf()
@@ -431,12 +436,14 @@ def run(mesh: Mesh, state: FieldState, t_end: float, t: float = 0.0, step: int =
                               L.ptr(state.qy), C.byref(tt), C.byref(ss), t_end, snapshot_interval,
                               max_steps, device, L.ptr(series), max_rows, C.byref(n_rows),
                               L.ptr(stats), L.ptr(snaps) if snapshots else None, len(snaps),
-                              C.byref(n_snaps), err, len(err))
+                              C.byref(n_snaps), L.ptr(fields), err, len(err))
     if rc:
         _raise(rc, err.value)
-    return RunResult(tt.value, ss.value, series[:min(n_rows.value, max_rows)].copy(),
-                     dict(zip(STAT_KEYS, stats.tolist())),
-                     snaps[:n_snaps.value].tolist() if snapshots else [])
+    res = RunResult(tt.value, ss.value, series[:min(n_rows.value, max_rows)].copy(),
+                    dict(zip(STAT_KEYS, stats.tolist())),
+                    snaps[:min(n_snaps.value, len(snaps))].tolist() if snapshots else [])
+    res.fields = fields[:min(n_snaps.value, snapshot_fields)] if snapshot_fields else None
+    return res
 
 
 # ---------------------------------------------------------------------------

@@ -323,8 +323,8 @@ EXPORT int swe_api_advance(void* mp, const double* params, double* h, double* qx
 EXPORT int swe_api_run(void* mp, const double* params, double* h, double* qx, double* qy,
                        double* t, long* step, double t_end, double snapshot_interval,
                        long max_steps, int device, double* series, long max_rows, long* n_rows,
-                       double* stats, double* snaps, long max_snaps, long* n_snaps, char* err,
-                       int errlen) {
+                       double* stats, double* snaps, long max_snaps, long* n_snaps,
+                       double* snap_fields, char* err, int errlen) {
   const auto& m = *static_cast<swe::Mesh*>(mp);
   swe::Simulation sim;
   sim.current = state_from(m.n_cells(), h, qx, qy);
@@ -337,8 +337,16 @@ EXPORT int swe_api_run(void* mp, const double* params, double* h, double* qx, do
   opt.max_steps = max_steps;
   long ns = 0;
   if (snaps)
-    opt.on_snapshot = [&](const swe::FieldState&, double tt, long) {
-      if (ns < max_snaps) snaps[ns] = tt;
+    opt.on_snapshot = [&](const swe::FieldState& f, double tt, long) {
+      if (ns < max_snaps) {
+        snaps[ns] = tt;
+        if (snap_fields) {  // [max_snaps][3][C]
+          const size_t C = f.h.size();
+          std::memcpy(snap_fields + (3 * ns + 0) * C, f.h.data(), C * sizeof(double));
+          std::memcpy(snap_fields + (3 * ns + 1) * C, f.qx.data(), C * sizeof(double));
+          std::memcpy(snap_fields + (3 * ns + 2) * C, f.qy.data(), C * sizeof(double));
+        }
+      }
       ++ns;
     };
   int rc = 0;

@@ -91,6 +91,10 @@ struct swe_dev_ctx {
   bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
+  // asynchronous snapshots: device staging slots, copy stream, events
+  double* snap[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t snap_ready[2] = {nullptr, nullptr}, snap_done[2] = {nullptr, nullptr};
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -651,6 +655,13 @@ int swe_dev_destroy(swe_dev_ctx* x) {
   for (void* p : x->allocs) cudaFree(p);
   for (void* p : x->link_allocs) cudaFree(p);
   for (void* p : x->ipc_mapped) cudaIpcCloseMemHandle(p);
+  if (x->copy_stream) cudaStreamSynchronize(x->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    for (int k = 0; k < 3; ++k) cudaFree(x->snap[i][k]);
+    if (x->snap_ready[i]) cudaEventDestroy(x->snap_ready[i]);
+    if (x->snap_done[i]) cudaEventDestroy(x->snap_done[i]);
+  }
+  if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
   cudaFree(x->halo_send);
   cudaFree(x->halo_recv);
   if (x->h_ctl) cudaFreeHost(x->h_ctl);
@@ -1214,6 +1225,68 @@ int swe_dev_last_record(swe_dev_ctx* x, swe_step_record* rec, swe_status* st) {
   if (code == SWE_OK && rec && x->h_ctl->n_rec > 0)
     CK(cudaMemcpy(rec, x->rec, sizeof(swe_step_record), cudaMemcpyDeviceToHost));
   return code;
+}
+
+// ---------------------------------------------------------------------------
+// asynchronous snapshots (reference run() on_snapshot, engine.hpp:347-379)
+// ---------------------------------------------------------------------------
+int swe_dev_snapshot_async(swe_dev_ctx* x, int slot, double* h, double* qx, double* qy) {
+  if (!x || slot < 0 || slot > 1 || !h || !qx || !qy)
+    return fail_invalid("swe_dev_snapshot_async: bad argument");
+  const int C = x->d.C;
+  CK(cudaSetDevice(x->device));
+  if (!x->copy_stream) {
+    CK(cudaStreamCreateWithFlags(&x->copy_stream, cudaStreamNonBlocking));
+    for (int i = 0; i < 2; ++i) {
+      CK(cudaEventCreateWithFlags(&x->snap_ready[i], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&x->snap_done[i], cudaEventDisableTiming));
+    }
+  }
+  if (!x->snap[slot][0])
+    for (int k = 0; k < 3; ++k) CK(cudaMalloc(&x->snap[slot][k], sizeof(double) * C));
+  // the slot's previous copy must be done before it is overwritten
+  CK(cudaStreamWaitEvent(x->stream, x->snap_done[slot], 0));
+  k_snapshot<<<blocks_for(C), kBlock, 0, x->stream>>>(x->d, x->snap[slot][0], x->snap[slot][1],
+                                                      x->snap[slot][2]);
+  ++g_launches;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(x->snap_ready[slot], x->stream));
+  CK(cudaStreamWaitEvent(x->copy_stream, x->snap_ready[slot], 0));
+  double* dst[3] = {h, qx, qy};
+  for (int k = 0; k < 3; ++k)
+    CK(cudaMemcpyAsync(dst[k], x->snap[slot][k], sizeof(double) * C, cudaMemcpyDeviceToHost,
+                       x->copy_stream));
+  CK(cudaEventRecord(x->snap_done[slot], x->copy_stream));
+  return SWE_OK;
+}
+
+int swe_dev_snapshot_wait(swe_dev_ctx* x, int slot) {
+  if (!x || slot < 0 || slot > 1) return fail_invalid("swe_dev_snapshot_wait: bad argument");
+  if (!x->snap_done[slot]) return SWE_OK;
+  CK(cudaEventSynchronize(x->snap_done[slot]));
+  return SWE_OK;
+}
+
+void* swe_dev_host_alloc(long long bytes) {
+  void* p = nullptr;
+  if (bytes <= 0 || cudaMallocHost(&p, (size_t)bytes) != cudaSuccess) return nullptr;
+  return p;
+}
+
+void swe_dev_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int swe_dev_host_register(void* p, long long bytes) {
+  if (!p || bytes <= 0) return fail_invalid("swe_dev_host_register: bad argument");
+  CK(cudaHostRegister(p, (size_t)bytes, cudaHostRegisterDefault));
+  return SWE_OK;
+}
+
+int swe_dev_host_unregister(void* p) {
+  if (!p) return SWE_OK;
+  CK(cudaHostUnregister(p));
+  return SWE_OK;
 }
 
 void* swe_dev_stream(swe_dev_ctx* x) { return x ? (void*)x->stream : nullptr; }

@@ -198,6 +198,17 @@ __global__ void k_state_out(int C, const int* c_new, const double* dh, const dou
   qy[o] = dqy[c];
 }
 
+// current state (buffer chosen on the device, for snapshots enqueued behind
+// asynchronous launches) -> reference order
+__global__ void k_snapshot(Dev d, double* h, double* qx, double* qy) {
+  const int o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= d.C) return;
+  const int cur = d.ctl->cur, c = d.c_new[o];
+  h[o] = d.h[cur][c];
+  qx[o] = d.qx[cur][c];
+  qy[o] = d.qy[cur][c];
+}
+
 // edge records -> reference left/right Flux3 arrays (compute_fluxes layout)
 __global__ void k_flux_out(Dev d, double* left, double* right) {
   const int e = blockIdx.x * blockDim.x + threadIdx.x;

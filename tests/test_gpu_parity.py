@@ -369,3 +369,26 @@ def test_advance_async_equals_advance():
     sb, _, _ = b.get_state()
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(sa, k), getattr(sb, k)), k
+
+
+@pytest.mark.parametrize("sync", [False, True], ids=["async", "sync"])
+def test_run_snapshots_are_the_states_at_their_steps(coracle, monkeypatch, sync):
+    """run()'s snapshots (copied D2H while the next segment already steps)
+    equal the oracle's state at the snapshot's step, bit for bit."""
+    if sync:
+        monkeypatch.setenv("SWE_SYNC_SNAPSHOTS", "1")
+    sc = api.make_scenario("three_mounds_friction", scale=0.05)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    st = sc.state.copy()
+    r = api.run(mesh, st, t_end=6.0, snapshot_interval=1.0, snapshots=True, snapshot_fields=8)
+    assert len(r.snapshots) == 7 and r.snapshots[0] == 0.0 and r.snapshots[-1] == 6.0
+    steps = {t: int(s) for s, t in r.series[:, :2]}
+    m = MeshArrays.from_mesh(mesh)
+    for ts, f in zip(r.snapshots[1:], r.fields[1:]):
+        k = steps[ts]
+        o = coracle.advance(m, sc.state.h, sc.state.qx, sc.state.qy, t_end=6.0, nsteps=k)
+        for j, key in enumerate(("h", "qx", "qy")):
+            assert bit_equal(f[j], o[key]), (ts, key)
+    o = coracle.advance(m, sc.state.h, sc.state.qx, sc.state.qy, t_end=6.0, nsteps=10**6,
+                        stop_at_t_end=True)
+    assert bit_equal(st.h, o["h"]) and r.step == o["step"]
