@@ -150,11 +150,13 @@ def load_peaks():
     return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def build_workload(name, scale):
+def build_workload(name, scale, device=None):
+    """scenario (host) + build_mesh (on `device` when given: swe_dev_build_mesh,
+    bit-identical to the host build)"""
     from paper_1807_00672_b200 import api
     t0 = time.perf_counter()
     sc = api.make_scenario(name, scale=scale, unstructured=True)
-    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=device)
     return sc, mesh, time.perf_counter() - t0
 
 
@@ -230,7 +232,7 @@ def run_b200_dist(args, rank, local, world):
     from paper_1807_00672_b200 import api, dist
 
     scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
-    sc, mesh, setup_s = build_workload(args.config, scale)
+    sc, mesh, setup_s = build_workload(args.config, scale, device=local)
     part = dist.partition(mesh, world)
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
@@ -321,7 +323,7 @@ def run_b200(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return run_b200_dist(args, rank, local, world)
 
-    sc, mesh, setup_s = build_workload(args.config, args.scale)
+    sc, mesh, setup_s = build_workload(args.config, args.scale, device=local)
     C, E = mesh.n_cells, mesh.n_edges
     t0 = time.perf_counter()
     solver = api.DeviceSolver(mesh, device=local)

@@ -303,6 +303,64 @@ inline StepStats advance_step(Simulation& sim, const Mesh& mesh, const PhysParam
   return out;
 }
 
+/// build_mesh (mesh.hpp:121-240) computed on the GPU: the same Mesh, bit for
+/// bit, and the same mesh_error texts as the host build_mesh (SURVEY §8(f)
+/// row 3: the host version is a serial bucket walk, ~12 s at 10M cells).
+inline Mesh build_mesh_device(const RawMesh& raw, std::vector<double> bathymetry,
+                              std::vector<double> manning, int device = 0) {
+  const int nn = static_cast<int>(raw.nodes.size());
+  const int nc = static_cast<int>(raw.triangles.size());
+  if (static_cast<int>(bathymetry.size()) != nc || static_cast<int>(manning.size()) != nc)
+    throw mesh_error("build_mesh: bathymetry/manning arrays must have one entry per triangle (got " +
+                     std::to_string(bathymetry.size()) + "/" + std::to_string(manning.size()) +
+                     " for " + std::to_string(nc) + " triangles)");
+  for (int c = 0; c < nc; ++c)
+    if (manning[c] < 0.0)
+      throw mesh_error("build_mesh: negative Manning coefficient at cell " + std::to_string(c));
+  static_assert(sizeof(Vec2) == 2 * sizeof(double) && sizeof(std::array<int, 3>) == 3 * sizeof(int),
+                "contiguous node / triangle arrays");
+  swe_built_mesh* b = nullptr;
+  char err[512] = {0};
+  const int rc = swe_dev_build_mesh(device, nn, reinterpret_cast<const double*>(raw.nodes.data()), nc,
+                                    reinterpret_cast<const int*>(raw.triangles.data()), &b, err,
+                                    sizeof(err));
+  if (rc == SWE_INVALID) throw mesh_error(err);
+  if (rc != SWE_OK) throw device_error(std::string("build_mesh_device: ") + swe_dev_last_error());
+  struct Guard {
+    swe_built_mesh* b;
+    ~Guard() { swe_dev_built_free(b); }
+  } guard{b};
+  int ne = 0;
+  swe_dev_built_sizes(b, nullptr, nullptr, &ne);
+  Mesh m;
+  m.nodes = raw.nodes;
+  m.cell_nodes.resize(nc);
+  m.cell_area.resize(nc);
+  m.cell_centroid.resize(nc);
+  m.cell_inradius.resize(nc);
+  m.cell_bed = std::move(bathymetry);
+  m.cell_manning = std::move(manning);
+  m.cell_edges.resize(nc);
+  m.edge_nodes.resize(ne);
+  m.edge_left.resize(ne);
+  m.edge_right.resize(ne);
+  m.edge_normal.resize(ne);
+  m.edge_length.resize(ne);
+  std::vector<double> cx(nc), cy(nc), nx(ne), ny(ne);
+  std::vector<int> ce(3 * (size_t)nc), cs(3 * (size_t)nc);
+  if (swe_dev_built_export(b, reinterpret_cast<int*>(m.cell_nodes.data()), m.cell_area.data(),
+                           cx.data(), cy.data(), m.cell_inradius.data(), ce.data(), cs.data(),
+                           reinterpret_cast<int*>(m.edge_nodes.data()), m.edge_left.data(),
+                           m.edge_right.data(), nx.data(), ny.data(), m.edge_length.data()) != SWE_OK)
+    throw device_error(std::string("build_mesh_device: ") + swe_dev_last_error());
+  for (int c = 0; c < nc; ++c) {
+    m.cell_centroid[c] = {cx[c], cy[c]};
+    for (int k = 0; k < 3; ++k) m.cell_edges[c][k] = {ce[3 * (size_t)c + k], cs[3 * (size_t)c + k]};
+  }
+  for (int e = 0; e < ne; ++e) m.edge_normal[e] = {nx[e], ny[e]};
+  return m;
+}
+
 /// The time loop (engine.hpp:335-394) with the state resident on the device.
 inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
                     const BackendSpec& backend, const RunOptions& opt) {

@@ -245,6 +245,21 @@ SWE_API long long swe_dev_launch_count(void);
 SWE_API int swe_dev_point_eval(int kind, long long n, const swe_params* params, const double* l,
                        const double* r, const double* z, const double* nrm, double* out);
 
+/* build_mesh (mesh.hpp:121-240) on the device: same numbering, geometry and
+ * error texts as the host build_mesh (include/swe/mesh.hpp).  xy [2*n_nodes],
+ * tris [3*n_cells].  SWE_INVALID with the reference's mesh_error text in err.
+ * Export arrays (any may be NULL): cell_nodes/cell_edge/cell_sign [3C],
+ * area/cx/cy/inradius [C], edge_nodes [2E], edge_left/right, nx/ny/len [E]. */
+typedef struct swe_built_mesh swe_built_mesh;
+SWE_API int swe_dev_build_mesh(int device, int n_nodes, const double* xy, int n_cells,
+                               const int* tris, swe_built_mesh** out, char* err, int errlen);
+SWE_API int swe_dev_built_sizes(swe_built_mesh* mesh, int* n_nodes, int* n_cells, int* n_edges);
+SWE_API int swe_dev_built_export(swe_built_mesh* mesh, int* cell_nodes, double* area, double* cx,
+                                 double* cy, double* inradius, int* cell_edge, int* cell_sign,
+                                 int* edge_nodes, int* edge_left, int* edge_right, double* nx,
+                                 double* ny, double* len);
+SWE_API void swe_dev_built_free(swe_built_mesh* mesh);
+
 SWE_API const char* swe_dev_strerror(int code);
 /* Last CUDA/argument error message of this thread. */
 SWE_API const char* swe_dev_last_error(void);

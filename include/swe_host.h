@@ -75,6 +75,11 @@ SWE_API void swe_host_local_plan(void* local, int* peers, int* send_counts, int*
                                  int* send_cells, int* recv_cells);
 SWE_API void swe_host_local_free(void* local);
 
+/* build_mesh on the GPU (include/swe/engine.hpp build_mesh_device): the same
+ * Mesh handle as swe_host_build_mesh, computed by swe_dev_build_mesh. */
+SWE_API void* swe_host_build_mesh_device(void* raw, const double* bed, const double* manning,
+                                         int device, char* err, int errlen);
+
 /* SWEMESH 1 mesh files (include/swe/swemesh.hpp; reference io.hpp:80-165):
  * parallel parse / format, the reference's values and error texts.  A file
  * handle owns a raw mesh (borrowed by swe_host_swemesh_raw, usable with

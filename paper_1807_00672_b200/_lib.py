@@ -115,6 +115,13 @@ _SIGS = {
     "swe_host_scenario_fields": (None, [c_void_p] + [c_void_p] * 5),
     "swe_host_scenario_free": (None, [c_void_p]),
     "swe_host_build_mesh": (c_void_p, [c_void_p, c_void_p, c_void_p, c_char_p, c_int]),
+    "swe_host_build_mesh_device": (c_void_p, [c_void_p, c_void_p, c_void_p, c_int, c_char_p,
+                                              c_int]),
+    "swe_dev_build_mesh": (c_int, [c_int, c_int, c_void_p, c_int, c_void_p, C.POINTER(c_void_p),
+                                   c_char_p, c_int]),
+    "swe_dev_built_sizes": (c_int, [c_void_p, P_int, P_int, P_int]),
+    "swe_dev_built_export": (c_int, [c_void_p] + [c_void_p] * 13),
+    "swe_dev_built_free": (None, [c_void_p]),
     "swe_host_mesh_sizes": (None, [c_void_p, P_int, P_int, P_int]),
     "swe_host_mesh_export": (None, [c_void_p] + [c_void_p] * 13),
     "swe_host_mesh_free": (None, [c_void_p]),

@@ -253,15 +253,21 @@ class Mesh:
         return v
 
 
-def build_mesh(raw: RawMesh, bathymetry, manning) -> Mesh:
-    """mesh.hpp:121-240 (re-implemented in include/swe/mesh.hpp)."""
+def build_mesh(raw: RawMesh, bathymetry, manning, device: int | None = None) -> Mesh:
+    """mesh.hpp:121-240 (re-implemented in include/swe/mesh.hpp); device=k:
+    computed on GPU k (swe_dev_build_mesh) -- the same Mesh bit for bit."""
     bed = np.ascontiguousarray(bathymetry, dtype=np.float64)
     man = np.ascontiguousarray(manning, dtype=np.float64)
     err = _errbuf()
     if len(bed) != raw.n_cells or len(man) != raw.n_cells:
         raise MeshError(f"build_mesh: bathymetry/manning arrays must have one entry per triangle "
                         f"(got {len(bed)}/{len(man)} for {raw.n_cells} triangles)")
-    h = L.load().swe_host_build_mesh(raw.handle, L.ptr(bed), L.ptr(man), err, len(err))
+    lib = L.load()
+    if device is None:
+        h = lib.swe_host_build_mesh(raw.handle, L.ptr(bed), L.ptr(man), err, len(err))
+    else:
+        h = lib.swe_host_build_mesh_device(raw.handle, L.ptr(bed), L.ptr(man), device, err,
+                                           len(err))
     if not h:
         _raise(3, err.value)
     m = Mesh(h)

@@ -165,6 +165,19 @@ EXPORT void* swe_host_build_mesh(void* raw, const double* bed, const double* man
   }
 }
 
+EXPORT void* swe_host_build_mesh_device(void* raw, const double* bed, const double* man, int device,
+                                        char* err, int errlen) {
+  try {
+    const auto& r = *static_cast<swe::RawMesh*>(raw);
+    const size_t nc = r.triangles.size();
+    return new swe::Mesh(swe::build_mesh_device(r, std::vector<double>(bed, bed + nc),
+                                                std::vector<double>(man, man + nc), device));
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return nullptr;
+  }
+}
+
 EXPORT void swe_host_mesh_sizes(void* p, int* nc, int* ne, int* nb) {
   const auto& m = *static_cast<swe::Mesh*>(p);
   *nc = m.n_cells();

@@ -12,8 +12,10 @@
 // node over the step.
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
@@ -22,6 +24,7 @@
 #include <string>
 #include <vector>
 
+#include "swe_build.cuh"
 #include "swe_ctl.cuh"
 #include "swe_dev.h"
 #include "swe_prep.cuh"
@@ -1288,6 +1291,247 @@ int swe_dev_host_unregister(void* p) {
   CK(cudaHostUnregister(p));
   return SWE_OK;
 }
+
+// ---------------------------------------------------------------------------
+// build_mesh on the device (swe_build.cuh; reference mesh.hpp:121-240)
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+struct swe_built_mesh {
+  int device = 0, nn = 0, nc = 0, ne = 0;
+  std::vector<void*> allocs;
+  int *cn = nullptr, *ce = nullptr, *cs = nullptr, *en = nullptr, *el = nullptr, *er = nullptr;
+  double *area = nullptr, *cx = nullptr, *cy = nullptr, *inr = nullptr;
+  double *nx = nullptr, *ny = nullptr, *len = nullptr;
+  template <class V>
+  V* alloc(size_t n) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(1, n) * sizeof(V)) != cudaSuccess) return nullptr;
+    allocs.push_back(p);
+    return static_cast<V*>(p);
+  }
+  ~swe_built_mesh() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+namespace {
+void put_err(const std::string& m, char* err, int errlen) {
+  g_last_error = m;
+  if (err && errlen > 0) {
+    std::strncpy(err, m.c_str(), (size_t)errlen - 1);
+    err[errlen - 1] = 0;
+  }
+}
+double hnorm(double x, double y) { return std::sqrt(x * x + y * y); }
+}  // namespace
+
+extern "C" {
+
+int swe_dev_build_mesh(int device, int nn, const double* xy, int nc, const int* tris,
+                       swe_built_mesh** out, char* err, int errlen) {
+  if (!out || nn < 0 || nc < 0 || (nn && !xy) || (nc && !tris))
+    return fail_invalid("swe_dev_build_mesh: bad argument");
+  *out = nullptr;
+  const bool timing = std::getenv("SWE_BUILD_TIMING") != nullptr;
+  auto tick = [t0 = std::chrono::steady_clock::now(), timing](const char* what) mutable {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[build_mesh_device] %-10s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  };
+  CK(cudaSetDevice(device));
+  tick("set_device");
+  auto* b = new swe_built_mesh();
+  b->device = device;
+  b->nn = nn;
+  b->nc = nc;
+  auto bail = [&](int rc) {
+    delete b;
+    return rc;
+  };
+  cudaStream_t s = nullptr;
+  if (!cuda_ok(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream")) return bail(SWE_CUDA);
+  struct StreamGuard {
+    cudaStream_t s;
+    ~StreamGuard() { cudaStreamDestroy(s); }
+  } guard{s};
+  Temps tmp;
+  const long long n3 = 3LL * nc;
+  double* dxy = (double*)tmp.get(sizeof(double) * 2 * (size_t)std::max(1, nn));
+  int* dtri = (int*)tmp.get(sizeof(int) * (size_t)std::max(1LL, n3));
+  BuildErr* derr = (BuildErr*)tmp.get(sizeof(BuildErr));
+  b->cn = b->alloc<int>(n3);
+  b->area = b->alloc<double>(nc);
+  b->cx = b->alloc<double>(nc);
+  b->cy = b->alloc<double>(nc);
+  b->inr = b->alloc<double>(nc);
+  b->ce = b->alloc<int>(n3);
+  b->cs = b->alloc<int>(n3);
+  if (!dxy || !dtri || !derr || !b->cn || !b->inr || !b->cs) {
+    g_last_error = "swe_dev_build_mesh: cudaMalloc failed";
+    return bail(SWE_CUDA);
+  }
+  BuildErr h_err{INT_MAX, INT_MAX, INT_MAX, 0};
+  bool ok = (!nn || cuda_ok(cudaMemcpyAsync(dxy, xy, sizeof(double) * 2 * (size_t)nn,
+                                            cudaMemcpyHostToDevice, s), "upload")) &&
+            (!nc || cuda_ok(cudaMemcpyAsync(dtri, tris, sizeof(int) * (size_t)n3,
+                                            cudaMemcpyHostToDevice, s), "upload")) &&
+            cuda_ok(cudaMemcpyAsync(derr, &h_err, sizeof(h_err), cudaMemcpyHostToDevice, s), "upload");
+  if (!ok) return bail(SWE_CUDA);
+  tick("alloc+h2d");
+  // loop 1: cells (mesh.hpp:189-212)
+  if (nc) kb_cells<<<blocks_for(nc), kBlock, 0, s>>>(nn, nc, dxy, dtri, b->cn, b->area, b->cx, b->cy,
+                                                     b->inr, derr);
+  if (!cuda_ok(cudaMemcpyAsync(&h_err, derr, sizeof(h_err), cudaMemcpyDeviceToHost, s), "d2h") ||
+      !cuda_ok(cudaStreamSynchronize(s), "build cells"))
+    return bail(SWE_CUDA);
+  tick("cells");
+  if (h_err.cell != INT_MAX) {  // the reference's text for the first bad triangle
+    const int c = h_err.cell;
+    int t[3] = {tris[3 * (size_t)c], tris[3 * (size_t)c + 1], tris[3 * (size_t)c + 2]};
+    std::string m;
+    for (int k = 0; k < 3 && m.empty(); ++k)
+      if (t[k] < 0 || t[k] >= nn)
+        m = "build_mesh: node index " + std::to_string(t[k]) + " out of range in triangle " +
+            std::to_string(c);
+    if (m.empty() && (t[0] == t[1] || t[1] == t[2] || t[0] == t[2]))
+      m = "build_mesh: degenerate triangle " + std::to_string(c) + " repeats a node index";
+    if (m.empty()) m = "build_mesh: triangle " + std::to_string(c) + " has zero area";
+    put_err(m, err, errlen);
+    return bail(SWE_INVALID);
+  }
+  // incidences in (lower node, upper node, cell, local) order (mesh.hpp:214-246)
+  unsigned long long* k0 = (unsigned long long*)tmp.get(8 * (size_t)std::max(1LL, n3));
+  unsigned long long* k1 = (unsigned long long*)tmp.get(8 * (size_t)std::max(1LL, n3));
+  int* v0 = (int*)tmp.get(4 * (size_t)std::max(1LL, n3));
+  int* v1 = (int*)tmp.get(4 * (size_t)std::max(1LL, n3));
+  int* head = (int*)tmp.get(4 * (size_t)std::max(1LL, n3));
+  int* eid = (int*)tmp.get(4 * (size_t)std::max(1LL, n3));
+  if (!k0 || !k1 || !v0 || !v1 || !head || !eid) {
+    g_last_error = "swe_dev_build_mesh: cudaMalloc failed";
+    return bail(SWE_CUDA);
+  }
+  int ne = 0;
+  if (n3) {
+    kb_keys<<<blocks_for(n3), kBlock, 0, s>>>(nc, b->cn, k0, v0);
+    if (!radix_sort(tmp, k0, k1, v0, v1, (int)n3, 32 + bits_for(nn), s)) return bail(SWE_CUDA);
+    kb_heads<<<blocks_for(n3), kBlock, 0, s>>>(n3, k1, head);
+    size_t tb = 0;
+    cub::DeviceScan::InclusiveSum(nullptr, tb, head, eid, (int)n3, s);
+    void* store = tmp.get(tb);
+    if (!store || !cuda_ok(cub::DeviceScan::InclusiveSum(store, tb, head, eid, (int)n3, s), "scan"))
+      return bail(SWE_CUDA);
+    if (!cuda_ok(cudaMemcpyAsync(&ne, eid + n3 - 1, sizeof(int), cudaMemcpyDeviceToHost, s), "d2h") ||
+        !cuda_ok(cudaStreamSynchronize(s), "build keys"))
+      return bail(SWE_CUDA);
+  }
+  tick("sort+scan");
+  b->ne = ne;
+  b->en = b->alloc<int>(2 * (size_t)ne);
+  b->el = b->alloc<int>(ne);
+  b->er = b->alloc<int>(ne);
+  b->nx = b->alloc<double>(ne);
+  b->ny = b->alloc<double>(ne);
+  b->len = b->alloc<double>(ne);
+  if (!b->en || !b->len) {
+    g_last_error = "swe_dev_build_mesh: cudaMalloc failed";
+    return bail(SWE_CUDA);
+  }
+  if (n3) {
+    kb_edges<<<blocks_for(n3), kBlock, 0, s>>>(n3, k1, v1, head, eid, b->cn, dxy, b->en, b->el, b->er,
+                                               b->nx, b->ny, b->len, b->ce, b->cs, derr);
+    if (!cuda_ok(cudaMemcpyAsync(&h_err, derr, sizeof(h_err), cudaMemcpyDeviceToHost, s), "d2h") ||
+        !cuda_ok(cudaStreamSynchronize(s), "build edges"))
+      return bail(SWE_CUDA);
+  }
+  tick("edges");
+  if (h_err.run != INT_MAX) {  // the first bad run in sorted order (mesh.hpp:252-272)
+    const long long i = h_err.run;
+    const int w = (int)std::min<long long>(64, n3 - i);
+    std::vector<unsigned long long> kk(w);
+    std::vector<int> vv(w);
+    cudaMemcpy(kk.data(), k1 + i, 8 * (size_t)w, cudaMemcpyDeviceToHost);
+    cudaMemcpy(vv.data(), v1 + i, 4 * (size_t)w, cudaMemcpyDeviceToHost);
+    int cnt = 1;
+    while (cnt < w && kk[cnt] == kk[0]) ++cnt;
+    auto directed = [&](int v, int& a0, int& a1) {
+      int t[3];
+      cudaMemcpy(t, b->cn + 3 * (size_t)(v / 3), sizeof(t), cudaMemcpyDeviceToHost);
+      a0 = t[v % 3];
+      a1 = t[(v % 3 + 1) % 3];
+    };
+    int a0, a1;
+    directed(vv[0], a0, a1);
+    std::string m = "build_mesh: non-manifold edge (" + std::to_string(a0) + "," + std::to_string(a1) + ")";
+    if (cnt > 2)
+      m += " shared by " + std::to_string(cnt) + " triangles";
+    else
+      m += " traversed twice in the same direction; triangles " + std::to_string(vv[0] / 3) +
+           " and " + std::to_string(vv[1] / 3) + " overlap or are inconsistently oriented";
+    put_err(m, err, errlen);
+    return bail(SWE_INVALID);
+  }
+  if (nc) {  // closed-polygon identity (mesh.hpp:280-291)
+    kb_closure<<<blocks_for(nc), kBlock, 0, s>>>(nc, b->ce, b->cs, b->nx, b->ny, b->len, derr);
+    if (!cuda_ok(cudaMemcpyAsync(&h_err, derr, sizeof(h_err), cudaMemcpyDeviceToHost, s), "d2h") ||
+        !cuda_ok(cudaStreamSynchronize(s), "build closure"))
+      return bail(SWE_CUDA);
+  }
+  tick("closure");
+  if (h_err.closure != INT_MAX) {
+    const int c = h_err.closure;
+    int ce[3], cs[3];
+    cudaMemcpy(ce, b->ce + 3 * (size_t)c, sizeof(ce), cudaMemcpyDeviceToHost);
+    cudaMemcpy(cs, b->cs + 3 * (size_t)c, sizeof(cs), cudaMemcpyDeviceToHost);
+    double sx = 0.0, sy = 0.0;
+    for (int k = 0; k < 3; ++k) {
+      double l, nxv, nyv;
+      cudaMemcpy(&l, b->len + ce[k], 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&nxv, b->nx + ce[k], 8, cudaMemcpyDeviceToHost);
+      cudaMemcpy(&nyv, b->ny + ce[k], 8, cudaMemcpyDeviceToHost);
+      const double t = cs[k] * l;
+      sx = sx + t * nxv;
+      sy = sy + t * nyv;
+    }
+    put_err("build_mesh: cell " + std::to_string(c) +
+                " fails the closed-polygon identity (residual " + std::to_string(hnorm(sx, sy)) + ")",
+            err, errlen);
+    return bail(SWE_INVALID);
+  }
+  *out = b;
+  return SWE_OK;
+}
+
+int swe_dev_built_sizes(swe_built_mesh* b, int* n_nodes, int* n_cells, int* n_edges) {
+  if (!b) return fail_invalid("null mesh");
+  if (n_nodes) *n_nodes = b->nn;
+  if (n_cells) *n_cells = b->nc;
+  if (n_edges) *n_edges = b->ne;
+  return SWE_OK;
+}
+
+int swe_dev_built_export(swe_built_mesh* b, int* cell_nodes, double* area, double* cx, double* cy,
+                         double* inradius, int* cell_edge, int* cell_sign, int* edge_nodes,
+                         int* edge_left, int* edge_right, double* nx, double* ny, double* len) {
+  if (!b) return fail_invalid("null mesh");
+  CK(cudaSetDevice(b->device));
+  const size_t C = (size_t)b->nc, E = (size_t)b->ne;
+  auto get = [&](void* dst, const void* src, size_t bytes) {
+    return !dst || !bytes || cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost) == cudaSuccess;
+  };
+  const bool ok = get(cell_nodes, b->cn, 12 * C) && get(area, b->area, 8 * C) &&
+                  get(cx, b->cx, 8 * C) && get(cy, b->cy, 8 * C) && get(inradius, b->inr, 8 * C) &&
+                  get(cell_edge, b->ce, 12 * C) && get(cell_sign, b->cs, 12 * C) &&
+                  get(edge_nodes, b->en, 8 * E) && get(edge_left, b->el, 4 * E) &&
+                  get(edge_right, b->er, 4 * E) && get(nx, b->nx, 8 * E) && get(ny, b->ny, 8 * E) &&
+                  get(len, b->len, 8 * E);
+  if (!ok) return cuda_ok(cudaGetLastError(), "swe_dev_built_export") ? SWE_CUDA : SWE_CUDA;
+  return SWE_OK;
+}
+
+void swe_dev_built_free(swe_built_mesh* b) { delete b; }
 
 void* swe_dev_stream(swe_dev_ctx* x) { return x ? (void*)x->stream : nullptr; }
 
