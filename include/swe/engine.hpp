@@ -25,6 +25,7 @@
 #include <vector>
 
 #include "swe/core.hpp"
+#include "swe/kernels.hpp"
 #include "swe/mesh.hpp"
 #include "swe_dev.h"
 

@@ -74,6 +74,27 @@ def build_api_driver(verbose: bool = False, force: bool = False) -> Path:
     return out
 
 
+JSON_INC = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/"
+                "thirdparty/nlohmann")
+REF_INC = Path("/root/reference/proj/include")
+
+
+def build_harness_driver(verbose: bool = False, force: bool = False) -> Path:
+    """The reference's own bench/convergence harness (its bench.hpp, included
+    in place) compiled against this repo's drop-in headers -- only where the
+    reference exists; the binary travels to the GPU box prebuilt."""
+    src = ROOT / "tests" / "cpp" / "harness_driver.cpp"
+    out = ROOT / "tests" / "cpp" / "harness_driver"
+    if not (REF_INC.exists() and (JSON_INC / "json.hpp").exists()):
+        return out
+    headers = list((INC / "swe").glob("*.hpp")) + list(INC.glob("*.h"))
+    if force or _stale(out, [src, LIB, *headers]):
+        _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", f"-I{INC}", f"-I{REF_INC}",
+              f"-I{JSON_INC}", src, "-o", out, f"-L{PKG}", "-lswe_b200",
+              "-Wl,-rpath,$ORIGIN/../../paper_1807_00672_b200"], verbose)
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     _run(["make", "-s", "-C", ROOT / "oracle"], verbose)
 
@@ -81,6 +102,7 @@ def build_oracle(verbose: bool = False) -> None:
 def build_all(verbose: bool = False, force: bool = False) -> None:
     build_library(verbose, force)
     build_api_driver(verbose, force)
+    build_harness_driver(verbose, force)
     build_oracle(verbose)
 
 
