@@ -70,6 +70,9 @@ def parse():
     return ap.parse_args()
 
 
+LOCKSTEP_CHECK = os.environ.get("SWE_BENCH_LOCKSTEP_CHECK") == "1"
+
+
 def dist_env():
     return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
             int(os.environ.get("WORLD_SIZE", "1")))
@@ -240,17 +243,33 @@ def run_b200_dist(args, rank, local, world):
     lp.set_state(sc.state)
     horizon = 1.7976931348623157e308
     W, K = max(3, args.warmup), args.steps
-    lp.advance(t_end=horizon, max_steps=W)
+    dev = "cpu" if LOCKSTEP_CHECK else "cuda"
+
+    def advance(target):  # run() segment up to step `target` (collective)
+        if LOCKSTEP_CHECK:
+            return dist.run_lockstep_ranks(lp, target - lp.clock()[1], t_end=horizon)
+        return lp.advance(t_end=horizon, max_steps=target)
+
+    def launch(target):
+        if LOCKSTEP_CHECK:
+            launch.recs = advance(target)
+        else:
+            lp.launch(t_end=horizon, max_steps=target)
+
+    def records():
+        return launch.recs if LOCKSTEP_CHECK else lp.records()
+
+    advance(W)
     # clocks ramp: keep stepping >= 1 s; every rank takes the same decision
     t_w = time.perf_counter()
     steps = W
     while True:
-        go = torch.tensor([1.0 if time.perf_counter() - t_w < 1.0 else 0.0], device="cuda")
+        go = torch.tensor([1.0 if time.perf_counter() - t_w < 1.0 else 0.0], device=dev)
         tdist.all_reduce(go, op=tdist.ReduceOp.MAX)
         if go.item() == 0.0:
             break
         steps += 50
-        lp.advance(t_end=horizon, max_steps=steps)
+        advance(steps)
     stream = torch.cuda.ExternalStream(dist_stream(lp), device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tdist.barrier()
@@ -258,15 +277,15 @@ def run_b200_dist(args, rank, local, world):
     clk = ClockSampler(local).start() if rank == 0 else None
     w0 = time.time()
     ev0.record(stream)
-    lp.launch(t_end=horizon, max_steps=steps + K)  # one graph launch per rank, no host sync
+    launch(steps + K)  # one graph launch per rank, no host sync
     ev1.record(stream)
     torch.cuda.synchronize()
-    recs = lp.records()
+    recs = records()
     if clk:
         clk.mark(w0, time.time())
         clk.stop()
     assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
-    ms = torch.tensor([ev0.elapsed_time(ev1)], device="cuda")
+    ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     ms = float(ms.item())
     C = mesh.n_cells
@@ -274,10 +293,10 @@ def run_b200_dist(args, rank, local, world):
     tdist.barrier()
     t0 = time.perf_counter()
     lp.set_state(sc.state)
-    lp.advance(t_end=horizon, max_steps=K)
+    advance(K)
     got = api.FieldState.zeros(C)
     lp.gather_owned(got)
-    e2e_s = torch.tensor([time.perf_counter() - t0], device="cuda")
+    e2e_s = torch.tensor([time.perf_counter() - t0], device=dev)
     tdist.all_reduce(e2e_s, op=tdist.ReduceOp.MAX)
     if rank == 0:
         out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
@@ -300,6 +319,9 @@ def run_b200_dist(args, rank, local, world):
                        "path": "LinkedPart.set_state (host) + advance (K steps, records D2H) + "
                                "gather_owned (host), max over ranks"},
                "step_dt_last": float(recs[-1, 2])}
+        if LOCKSTEP_CHECK:
+            out = {"lockstep_check": True, "note": "N>1 code path validated on one GPU; "
+                   "not a bench value", "records_ok": bool(len(recs) == K), **out}
         print(json.dumps(out))
     tdist.barrier()
     lp.close()
@@ -318,6 +340,13 @@ def run_b200(args):
     rank, local, world = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device (the B200 path has no CPU fallback)")
+    if world > 1 and LOCKSTEP_CHECK:
+        # validation of the N>1 path on ONE GPU: every rank on device 0, gloo,
+        # barrier-separated lockstep phases (no kernel waits on a concurrently
+        # running one); the numbers it prints are not bench values
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo")
+        return run_b200_dist(args, rank, 0, world)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))

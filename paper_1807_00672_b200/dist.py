@@ -7,19 +7,23 @@ step) + every edge touching an owned cell, so cut edges are evaluated by both
 sides from identical inputs and a P-part run is bit-identical to the
 single-domain run (only the per-step mass is summed in a different order).
 
-Per step (driver: ``run_parts``):
+Production path -- LINKED contexts (``LinkedPart``, ``link_torch`` /
+``link_local``): the step kernel pushes the new state of the cells a peer
+holds as ghosts straight into that peer's buffers (CUDA IPC peer memory over
+NVLink) and the CFL bound / step outcome is exchanged through device
+mailboxes, all inside each rank's CUDA graph: no host round trip per step.
+``run_lockstep`` / ``run_lockstep_ranks`` step linked parts phase by phase
+(several parts sharing one device; tests).
+
+Host-driven building blocks (``PartSolver`` + ``run_parts``), kept for the
+CPU protocol tests (gloo): per step
   1. halo exchange: each part packs the owned cells its peers need (3 doubles
-     per cell, device buffer), the buffers move peer-to-peer, each part
-     unpacks into its ghosts;
+     per cell), the buffers move peer-to-peer, each part unpacks into its ghosts;
   2. global CFL bound: min over parts of the local bound, max of max_speed;
   3. every part takes the step with the global bound.
-
-Exchange backends:
-  ``LocalExchange``  all parts in this process (one or several GPUs):
-                     device-to-device copies of the packed blocks.
-  ``TorchExchange``  one part per rank (torchrun): torch.distributed
-                     batch_isend_irecv (NCCL over NVLink on GPUs, gloo on CPU)
-                     + all_reduce(MIN/MAX) for the CFL bound.
+  ``LocalExchange``  all parts in this process: device-to-device copies.
+  ``TorchExchange``  one part per rank: torch.distributed batch_isend_irecv
+                     + all_reduce(MIN/MAX).
 """
 from __future__ import annotations
 
@@ -363,6 +367,12 @@ class LinkedPart:
         own = self.lm.cells[:self.lm.n_owned]
         no = self.lm.n_owned
         out.h[own], out.qx[own], out.qy[own] = h[:no], qx[:no], qy[:no]
+        return t.value, step.value
+
+    def clock(self):
+        t, step = C.c_double(), C.c_longlong()
+        _check(self.lib.swe_dev_get_state(self.ctx, None, None, None, C.byref(t), C.byref(step)),
+               "swe_dev_get_state")
         return t.value, step.value
 
     def ledger(self):
