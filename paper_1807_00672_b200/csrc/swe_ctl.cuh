@@ -126,6 +126,12 @@ struct Dev {
   const int* eoff;  // [ntiles+1] owned edge range of each tile
   const int* hoff;  // [ntiles+1] halo list range of each tile
   const int* halo;  // halo edges (owned by another tile, touching this one)
+  // staged tiles (k_tile_s): every slot (owned + halo edge) of every tile in
+  // tile order, so a tile's slot data is one contiguous range [soff[t], soff[t+1])
+  int stage;
+  const int* soff;
+  const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
+  const double *snx, *sny, *slen;
   // state, double-buffered
   double *h[2], *qx[2], *qy[2];
   // per-incidence contributions [3C] of the two-phase step

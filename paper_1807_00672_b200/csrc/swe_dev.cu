@@ -122,7 +122,12 @@ struct swe_dev_ctx {
 
 namespace {
 
-const void* tile_kernel(int threads, bool link) {
+const void* tile_kernel(int threads, bool link, bool stage = false) {
+  if (stage) {
+    if (threads == 128)
+      return link ? (const void*)k_tile_s<128, true> : (const void*)k_tile_s<128, false>;
+    return link ? (const void*)k_tile_s<256, true> : (const void*)k_tile_s<256, false>;
+  }
   if (threads == 128) return link ? (const void*)k_tile<128, true> : (const void*)k_tile<128, false>;
   return link ? (const void*)k_tile<256, true> : (const void*)k_tile<256, false>;
 }
@@ -133,6 +138,17 @@ int launch_update(swe_dev_ctx* x) {
     const bool L = x->linked;
     const int g = x->grid_tile;
     const size_t sm = x->tile_smem;
+    if (x->d.stage) {
+      if (x->tile_threads == 128) {
+        if (L) k_tile_s<128, true><<<g, 128, sm, x->stream>>>(x->d);
+        else k_tile_s<128, false><<<g, 128, sm, x->stream>>>(x->d);
+      } else {
+        if (L) k_tile_s<256, true><<<g, 256, sm, x->stream>>>(x->d);
+        else k_tile_s<256, false><<<g, 256, sm, x->stream>>>(x->d);
+      }
+      ++g_launches;
+      return cuda_ok(cudaGetLastError(), "k_tile_s") ? SWE_OK : SWE_CUDA;
+    }
     if (x->tile_threads == 128) {
       if (L) k_tile<128, true><<<g, 128, sm, x->stream>>>(x->d);
       else k_tile<128, false><<<g, 128, sm, x->stream>>>(x->d);
@@ -518,7 +534,9 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   // tile size: at most 256 cells (measured best, r02), shrunk so the tiles
   // fill whole waves of the persistent grid (a 1.28M-cell part has 4.2 waves
   // of 256-cell tiles: the last one 23% busy)
-  int T = 256;
+  if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
+  const int t_max = d.stage ? 128 : 256;  // staged tiles: ~25 KB of shared memory at 128 cells
+  int T = t_max;
   if (const char* env = std::getenv("SWE_TILE_CELLS")) {
     T = std::max(32, std::atoi(env));
   } else {
@@ -529,9 +547,9 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, tile_kernel(x->tile_threads, false),
                                                   x->tile_threads, tile_smem_bytes(256, 0));
     const long long grid = (long long)sms * std::max(1, occ);
-    const long long waves = std::max(1LL, (d.C_own + 256 * grid - 1) / (256 * grid));
+    const long long waves = std::max(1LL, (d.C_own + t_max * grid - 1) / (t_max * grid));
     const long long t = (d.C_own + waves * grid - 1) / (waves * grid);
-    T = (int)std::min(256LL, std::max(32LL, (t + 7) / 8 * 8));
+    T = (int)std::min((long long)t_max, std::max(32LL, (t + 7) / 8 * 8));
     cudaGetLastError();
   }
   d.T = T;
@@ -600,6 +618,32 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.rec = x->rec;
 
   if (int rc = preprocess(x, m)) return bail(rc);
+  if (d.stage) {  // slot arrays of the staged tile kernel
+    const size_t ns = (size_t)E + (size_t)x->n_halo;
+    int* soff = x->alloc<int>(d.ntiles + 1);
+    int* sel = x->alloc<int>(ns);
+    int* ser = x->alloc<int>(ns);
+    int* skk = x->alloc<int>(ns);
+    int* sedge = x->alloc<int>(ns);
+    double* snx = x->alloc<double>(ns);
+    double* sny = x->alloc<double>(ns);
+    double* slen = x->alloc<double>(ns);
+    if (!slen) {
+      g_last_error = "swe_dev_create: cudaMalloc (slot arrays) failed";
+      return bail(SWE_CUDA);
+    }
+    k_slots<<<blocks_for(32LL * d.ntiles), kBlock, 0, x->stream>>>(d, soff, sel, ser, skk, sedge,
+                                                                  snx, sny, slen);
+    if (!cuda_ok(cudaGetLastError(), "k_slots")) return bail(SWE_CUDA);
+    d.soff = soff;
+    d.sel = sel;
+    d.ser = ser;
+    d.skk = skk;
+    d.sedge = sedge;
+    d.snx = snx;
+    d.sny = sny;
+    d.slen = slen;
+  }
 
   // grid sizes: resident blocks per SM x SM count (persistent grid-stride)
   int sms = 148;
@@ -607,7 +651,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   int occ_face = 0, occ_cell = 0, occ_tile = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_face, k_face_c, kBlock, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cell, k_cell_c, kBlock, 0);
-  x->tile_smem = tile_smem_bytes(d.T, d.max_slots);
+  x->tile_smem = d.stage ? tile_stage_smem_bytes(d.T, d.max_slots) : tile_smem_bytes(d.T, d.max_slots);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if ((long long)x->tile_smem + 1024 > smem_optin) {
@@ -616,9 +660,9 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
                    std::to_string(smem_optin) + "); use a smaller SWE_TILE_CELLS";
     return bail(SWE_INVALID);
   }
-  const void* ktile = tile_kernel(x->tile_threads, false);
+  const void* ktile = tile_kernel(x->tile_threads, false, d.stage);
   for (int L = 0; L < 2; ++L)
-    if (!cuda_ok(cudaFuncSetAttribute(tile_kernel(x->tile_threads, L),
+    if (!cuda_ok(cudaFuncSetAttribute(tile_kernel(x->tile_threads, L, d.stage),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)x->tile_smem),
                  "tile smem attribute"))

@@ -129,6 +129,30 @@ __global__ void k_halo_bounds(int nh, const unsigned long long* key, int ntiles,
     for (int u = t + 1; u <= ntiles; ++u) hoff[u] = nh;
 }
 
+// staged tiles: slot arrays in tile order (one warp per tile)
+__global__ void k_slots(Dev d, int* soff, int* sel, int* ser, int* skk, int* sedge, double* snx,
+                        double* sny, double* slen) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= d.ntiles) return;
+  const int e0 = d.eoff[t], no = d.eoff[t + 1] - e0;
+  const int h0 = d.hoff[t], ns = no + d.hoff[t + 1] - h0;
+  const int s0 = e0 + h0;  // slots before tile t: owned edges + halo edges before it
+  if (lane == 0) {
+    soff[t] = s0;
+    if (t == d.ntiles - 1) soff[t + 1] = s0 + ns;
+  }
+  for (int j = lane; j < ns; j += 32) {
+    const int e = j < no ? e0 + j : d.halo[h0 + (j - no)];
+    sel[s0 + j] = d.el[e];
+    ser[s0 + j] = d.er[e];
+    skk[s0 + j] = d.kl[e] | (d.kr[e] << 8);
+    sedge[s0 + j] = e;
+    snx[s0 + j] = d.nx[e];
+    sny[s0 + j] = d.ny[e];
+    slen[s0 + j] = d.len[e];
+  }
+}
+
 __global__ void k_fill_int(int n, int* v, int value) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = value;

@@ -382,4 +382,164 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
 }
 
+// ---------------------------------------------------------------------------
+// staged tile kernel (option, SWE_TILE_STAGE=1): every contiguous input of a
+// tile -- state, bed, area, n, r of its cells and the per-tile slot arrays
+// (owned + halo edges copied in tile order at create) -- is brought into
+// shared memory by one batch of cp.async copies, so a tile costs one memory
+// round trip instead of several dependent ones.  128-cell tiles keep it at
+// ~25 KB per CTA (8 CTAs/SM, as the default kernel).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__host__ __device__ constexpr size_t tile_stage_smem_bytes(int T, int S) {
+  return sizeof(double) * (16 * (size_t)T + 3 * (size_t)S) + sizeof(int) * 3 * (size_t)S;
+}
+
+template <int NT, bool LINK>
+__global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile_s(Dev d) {
+  extern __shared__ double smem[];
+  Ctl* ctl = d.ctl;
+  if (!ctl->active) return;
+  const int cur = ctl->cur;
+  const double dt = step_dt(ctl, d.sp->t_end, nullptr);
+  const double* __restrict__ H = d.h[cur];
+  const double* __restrict__ QX = d.qx[cur];
+  const double* __restrict__ QY = d.qy[cur];
+  double* NH = d.h[cur ^ 1];
+  double* NQX = d.qx[cur ^ 1];
+  double* NQY = d.qy[cur ^ 1];
+  const int T = d.T, S = d.max_slots;
+  double* sh = smem;
+  double* sq = sh + T;
+  double* sr = sq + T;
+  double* sz = sr + T;
+  double* sa = sz + T;
+  double* sm = sa + T;
+  double* si = sm + T;
+  double* tm = si + T;
+  double* tx = tm + 3 * T;
+  double* ty = tx + 3 * T;
+  double* gnx = ty + 3 * T;
+  double* gny = gnx + S;
+  double* gln = gny + S;
+  int* gel = reinterpret_cast<int*>(gln + S);
+  int* ger = gel + S;
+  int* gkk = ger + S;
+  const Phys P = d.P;
+  CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
+
+  for (int t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+    const int c0 = t * T;
+    const int nc = min(T, d.C_own - c0);
+    const int s0 = __ldg(d.soff + t), ns = __ldg(d.soff + t + 1) - s0;
+    for (int i = threadIdx.x; i < nc; i += NT) {
+      cp_async8(sh + i, H + c0 + i);
+      cp_async8(sq + i, QX + c0 + i);
+      cp_async8(sr + i, QY + c0 + i);
+      cp_async8(sz + i, d.z + c0 + i);
+      cp_async8(sa + i, d.area + c0 + i);
+      cp_async8(sm + i, d.man + c0 + i);
+      cp_async8(si + i, d.inr + c0 + i);
+    }
+    for (int j = threadIdx.x; j < ns; j += NT) {
+      cp_async4(gel + j, d.sel + s0 + j);
+      cp_async4(ger + j, d.ser + s0 + j);
+      cp_async4(gkk + j, d.skk + s0 + j);
+      cp_async8(gnx + j, d.snx + s0 + j);
+      cp_async8(gny + j, d.sny + s0 + j);
+      cp_async8(gln + j, d.slen + s0 + j);
+    }
+    int p0 = 0, p1 = 0;
+    if (LINK) {
+      p0 = __ldg(d.L.tile_push + t);
+      p1 = __ldg(d.L.tile_push + t + 1);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+
+    for (int j = threadIdx.x; j < ns; j += NT) {
+      const int cl = gel[j], cr = ger[j];
+      const double nx = gnx[j], ny = gny[j], len = gln[j];
+      const bool w = cr < 0;
+      const int il = cl - c0, ir = (w ? cl : cr) - c0;
+      const bool inL = (unsigned)il < (unsigned)nc, inR = !w && (unsigned)ir < (unsigned)nc;
+      Cons uL, uR;
+      double zl, zr;
+      if (inL) {
+        uL = Cons{sh[il], sq[il], sr[il]};
+        zl = sz[il];
+      } else {
+        uL = Cons{__ldg(H + cl), __ldg(QX + cl), __ldg(QY + cl)};
+        zl = __ldg(d.z + cl);
+      }
+      if ((unsigned)ir < (unsigned)nc) {
+        uR = Cons{sh[ir], sq[ir], sr[ir]};
+        zr = sz[ir];
+      } else {
+        const int c = ir + c0;
+        uR = Cons{__ldg(H + c), __ldg(QX + c), __ldg(QY + c)};
+        zr = __ldg(d.z + c);
+      }
+      EdgeTerms et;
+      if (!edge_terms(uL, zl, uR, zr, w, nx, ny, len, P, et)) {
+        atomicMin(&ctl->bad_edge, __ldg(d.e_orig + __ldg(d.sedge + s0 + j)));
+        continue;
+      }
+      const int kk = gkk[j];
+      if (inL) {
+        const int s = 3 * il + (kk & 0xff);
+        tm[s] = et.lm;
+        tx[s] = et.lx;
+        ty[s] = et.ly;
+      }
+      if (inR) {
+        const int s = 3 * ir + (kk >> 8);
+        tm[s] = et.rm;
+        tx[s] = et.rx;
+        ty[s] = et.ry;
+      }
+    }
+    __syncthreads();
+
+    for (int i = threadIdx.x; i < nc; i += NT) {
+      double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
+#pragma unroll
+      for (int k = 0; k < 3; ++k) {
+        am += tm[3 * i + k];
+        ax += tx[3 * i + k];
+        ay += ty[3 * i + k];
+      }
+      const Cons u = cell_finish_v(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, sa[i], sm[i],
+                                   si[i], NH, NQX, NQY, a);
+      if (LINK && p1 > p0) {
+        sh[i] = u.h;
+        sq[i] = u.qx;
+        sr[i] = u.qy;
+      }
+    }
+    __syncthreads();
+    if (LINK && p1 > p0) {
+      for (int j = p0 + threadIdx.x; j < p1; j += NT) {
+        const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);
+        double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + j) + 3 * (cur ^ 1);
+        dst[0][g] = sh[i];
+        dst[1][g] = sq[i];
+        dst[2][g] = sr[i];
+      }
+      __threadfence_system();
+      __syncthreads();
+    }
+  }
+  block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
+}
+
 }  // namespace swe_b200

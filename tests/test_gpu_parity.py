@@ -392,3 +392,19 @@ def test_run_snapshots_are_the_states_at_their_steps(coracle, monkeypatch, sync)
     o = coracle.advance(m, sc.state.h, sc.state.qx, sc.state.qy, t_end=6.0, nsteps=10**6,
                         stop_at_t_end=True)
     assert bit_equal(st.h, o["h"]) and r.step == o["step"]
+
+
+def test_staged_tile_option_is_bit_identical(coracle, monkeypatch):
+    """SWE_TILE_STAGE=1 (cp.async-staged tiles) == oracle."""
+    monkeypatch.setenv("SWE_TILE_STAGE", "1")
+    sc = api.make_scenario("sloping_wet_dry", scale=0.03)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    s = api.DeviceSolver(m)
+    assert s.info()["tile_cells"] <= 128
+    s.set_state(sc.state)
+    recs = s.advance(1e30, max_steps=120)
+    got, _, _ = s.get_state()
+    o = coracle.advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy, nsteps=120)
+    assert bit_equal(recs[:, 2], o["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), o[k]), k
