@@ -179,3 +179,19 @@ def test_linked_ranks_over_cuda_ipc():
     for rank, own, h, qx, qy, _, _ in res:
         assert bit_equal(h, ref["h"][own]) and bit_equal(qx, ref["qx"][own])
         assert bit_equal(qy, ref["qy"][own])
+
+
+def test_linked_two_phase_single_rank_graph():
+    """linked two-phase step (k_face_c, k_cell_c, k_push, k_exchange) in the graph"""
+    sc, m, lms = _scenario_parts(1)
+    p = dist.LinkedPart(lms[0], two_phase=True)
+    dist.link_local([p])
+    p.set_state(sc.state)
+    recs = p.advance(max_steps=150)
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=150)
+    got = api.FieldState.zeros(m.n_cells)
+    p.gather_owned(got)
+    assert bit_equal(recs[:, 2], ref["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), ref[k]), k

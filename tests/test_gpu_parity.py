@@ -408,3 +408,55 @@ def test_staged_tile_option_is_bit_identical(coracle, monkeypatch):
     assert bit_equal(recs[:, 2], o["dts"])
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(got, k), o[k]), k
+
+
+def _square_case(nx, ny, seed, dry_frac=0.3):
+    raw = api.generate_square_mesh(nx, ny, float(nx), float(ny))
+    n = raw.n_cells
+    rng = np.random.default_rng(seed)
+    bed = rng.uniform(0.0, 0.3, n)
+    man = np.where(rng.random(n) < 0.5, 0.03, 0.0)
+    h = np.where(rng.random(n) < dry_frac, 0.0, rng.uniform(0.2, 2.0, n))
+    qx = np.where(h > 0, rng.uniform(-1, 1, n) * h, 0.0)
+    qy = np.where(h > 0, rng.uniform(-1, 1, n) * h, 0.0)
+    return api.build_mesh(raw, bed, man), api.FieldState(h, qx, qy)
+
+
+@pytest.mark.parametrize("nx,ny", [(1, 1), (1, 2), (2, 1), (3, 1), (5, 4)])
+def test_tiny_meshes_bitwise(coracle, nx, ny):
+    """the smallest meshes: every cell on the boundary, tiles of one cell"""
+    m, st = _square_case(nx, ny, seed=nx * 10 + ny)
+    s = api.DeviceSolver(m)
+    s.set_state(st)
+    recs = s.advance(1e30, max_steps=60)
+    got, _, _ = s.get_state()
+    o = coracle.advance(MeshArrays.from_mesh(m), st.h, st.qx, st.qy, nsteps=60)
+    assert bit_equal(recs[:, 2], o["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), o[k]), k
+
+
+def test_all_dry_domain_steps_with_dt_max(coracle):
+    """engine.hpp:214: every cell dry -> dt = dt_max, nothing moves"""
+    m, st = _square_case(20, 10, seed=3, dry_frac=1.0)
+    s = api.DeviceSolver(m)
+    s.set_state(st)
+    recs = s.advance(1e30, max_steps=5)
+    assert np.all(recs[:, 2] == api.PhysParams().dt_max) and np.all(recs[:, 4] == 0.0)
+    got, t, _ = s.get_state()
+    assert t == 5 * api.PhysParams().dt_max and not np.any(got.h) and not np.any(got.qx)
+
+
+def test_single_wet_cell_spreads_into_dry_cells(coracle):
+    """a wetting front from one cell: dry-bed HLLC branches and the clamp"""
+    m, st = _square_case(30, 30, seed=5, dry_frac=1.0)
+    st.h[450] = 2.0
+    s = api.DeviceSolver(m)
+    s.set_state(st)
+    recs = s.advance(1e30, max_steps=200)
+    got, _, _ = s.get_state()
+    o = coracle.advance(MeshArrays.from_mesh(m), st.h, st.qx, st.qy, nsteps=200)
+    assert bit_equal(recs[:, 2], o["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), o[k]), k
+    assert np.count_nonzero(got.h) > 50
