@@ -236,7 +236,7 @@ def run_b200_dist(args, rank, local, world):
 
     scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
     sc, mesh, setup_s = build_workload(args.config, scale, device=local)
-    part = dist.partition(mesh, world)
+    part = dist.partition(mesh, world, dist.cost_weights(sc.state))  # equal work per GPU
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
     dist.link_torch(lp)
@@ -303,11 +303,13 @@ def run_b200_dist(args, rank, local, world):
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args.config, sc, mesh, 1, {
-                   "parallelism": f"{world}-way RCB domain decomposition, one part per GPU; "
+                   "parallelism": f"{world}-way cost-weighted RCB domain decomposition (wet "
+                                  f"cells weighted {dist.WET_COST}x dry), one part per GPU; "
                                   "ghost states pushed peer-to-peer by the step kernel, CFL "
                                   "bound / outcome through device mailboxes (no host round "
                                   "trip per step)",
                    "cells_per_gpu_max": int(np.bincount(part).max()),
+                   "cells_per_gpu_min": int(np.bincount(part).min()),
                    "halo_cells_rank0": int(lm.n_cells - lm.n_owned), "setup_s": round(setup_s, 2)}),
                "gpu_launches": 2 * K + 2,
                "gpu_launches_note": "per rank: k_set_params + one CUDA-graph launch = k_gate + "

@@ -61,6 +61,9 @@ SWE_API void swe_host_mesh_free(void* mesh);
 /* domain decomposition (include/swe/partition.hpp): part id per cell by
  * recursive coordinate bisection */
 SWE_API int swe_host_partition(void* mesh, int nparts, int* part_out);
+/* the same with per-cell weights (equal weight per part; include/swe/partition.hpp
+ * cost_weights gives the step's measured cost of wet vs dry cells) */
+SWE_API int swe_host_partition_weighted(void* mesh, int nparts, const double* weights, int* part_out);
 /* part p's local mesh (owned cells first, then ghosts) and exchange plan */
 SWE_API void* swe_host_local_mesh(void* mesh, const int* part, int p, char* err, int errlen);
 SWE_API void swe_host_local_sizes(void* local, int* n_cells, int* n_owned, int* n_edges,

@@ -126,6 +126,7 @@ _SIGS = {
     "swe_host_mesh_export": (None, [c_void_p] + [c_void_p] * 13),
     "swe_host_mesh_free": (None, [c_void_p]),
     "swe_host_partition": (c_int, [c_void_p, c_int, c_void_p]),
+    "swe_host_partition_weighted": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "swe_host_local_mesh": (c_void_p, [c_void_p, c_void_p, c_int, c_char_p, c_int]),
     "swe_host_local_sizes": (None, [c_void_p] + [P_int] * 6),
     "swe_host_local_export": (None, [c_void_p] + [c_void_p] * 15),

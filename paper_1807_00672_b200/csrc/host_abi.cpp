@@ -410,6 +410,18 @@ EXPORT int swe_host_partition(void* mp, int nparts, int* part_out) {
   }
 }
 
+EXPORT int swe_host_partition_weighted(void* mp, int nparts, const double* weights, int* part_out) {
+  try {
+    const auto& m = *static_cast<swe::Mesh*>(mp);
+    const std::vector<double> w(weights, weights + m.n_cells());
+    const std::vector<int> p = swe::rcb_partition(m, nparts, &w);
+    std::memcpy(part_out, p.data(), sizeof(int) * p.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return kind_of(e);
+  }
+}
+
 EXPORT void* swe_host_local_mesh(void* mp, const int* part, int p, char* err, int errlen) {
   try {
     const auto& m = *static_cast<swe::Mesh*>(mp);

@@ -51,7 +51,7 @@ struct Ctl {
   int link_err;  // a peer exchange timed out (sticky until set_state)
   unsigned long long xseq;  // exchanges posted so far (linked contexts)
   unsigned int done;        // blocks of the running step kernel that finished
-  int pad2;
+  int tile_next;            // dynamic tile counter of k_tile (reset by finalize)
 };
 
 struct Part {  // one block's partial results
@@ -129,6 +129,7 @@ struct Dev {
   // staged tiles (k_tile_s): every slot (owned + halo edge) of every tile in
   // tile order, so a tile's slot data is one contiguous range [soff[t], soff[t+1])
   int stage;
+  int dyn;  // k_tile fetches tiles from a counter instead of round robin
   const int* soff;
   const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
   const double *snx, *sny, *slen;
@@ -306,6 +307,7 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   const StepParams* sp = d.sp;
   c->status = SWE_OK;
   c->n_rec = 0;
+  c->tile_next = 0;
   c->bad_edge = kNone;
   c->bad_cell = kNone;
   c->bad_speed = kNone;
@@ -344,6 +346,7 @@ __device__ __forceinline__ Ctl load_ctl(const Ctl* c) {
 __device__ void finalize_step(const Dev& d, const Part& p, int status, int index, double err_h,
                               cudaGraphConditionalHandle cond, int use_cond) {
   Ctl c = load_ctl(d.ctl);
+  c.tile_next = 0;
   const StepParams sp = *d.sp;
   const bool last = c.t + c.dts >= sp.t_end;  // engine.hpp:236-237
   const double dt = last ? sp.t_end - c.t : c.dts;

@@ -535,6 +535,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   // fill whole waves of the persistent grid (a 1.28M-cell part has 4.2 waves
   // of 256-cell tiles: the last one 23% busy)
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
+  if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
   const int t_max = d.stage ? 128 : 256;  // staged tiles: ~25 KB of shared memory at 128 cells
   int T = t_max;
   if (const char* env = std::getenv("SWE_TILE_CELLS")) {

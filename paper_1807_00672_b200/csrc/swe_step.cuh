@@ -287,7 +287,8 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   const Phys P = d.P;
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
-  for (int t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
+  __shared__ int s_next;
+  for (int t = blockIdx.x; t < d.ntiles;) {
     const int c0 = t * T;
     const int nc = min(T, d.C_own - c0);
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile
@@ -377,6 +378,13 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
       }
       __threadfence_system();
       __syncthreads();
+    }
+    if (d.dyn) {  // next tile from a shared counter (experiment, SWE_DYN_TILES=1)
+      if (threadIdx.x == 0) s_next = gridDim.x + atomicAdd(&ctl->tile_next, 1);
+      __syncthreads();
+      t = s_next;
+    } else {
+      t += gridDim.x;
     }
   }
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);

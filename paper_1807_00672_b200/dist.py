@@ -36,13 +36,30 @@ from . import _lib as L
 from .api import DeviceError, FieldState, Mesh, NumericError, PhysParams, _check, _errbuf, _raise
 
 
-def partition(mesh: Mesh, nparts: int) -> np.ndarray:
-    """part id per cell (recursive coordinate bisection of centroids)."""
+def partition(mesh: Mesh, nparts: int, weights=None) -> np.ndarray:
+    """part id per cell (recursive coordinate bisection of centroids); with
+    per-cell weights (cost_weights) the parts get equal work instead of equal
+    cell counts."""
     out = np.empty(mesh.n_cells, dtype=np.int32)
-    rc = L.load().swe_host_partition(mesh.handle, nparts, L.ptr(out))
+    lib = L.load()
+    if weights is None:
+        rc = lib.swe_host_partition(mesh.handle, nparts, L.ptr(out))
+    else:
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        if len(w) != mesh.n_cells:
+            raise ValueError("partition: one weight per cell required")
+        rc = lib.swe_host_partition_weighted(mesh.handle, nparts, L.ptr(w), L.ptr(out))
     if rc:
         _raise(rc, "rcb_partition failed")
     return out
+
+
+WET_COST = 1.65  # wet / dry cell step cost on B200 (tools/scaling_proxy.py)
+
+
+def cost_weights(state: FieldState, h_dry: float = 1e-6, wet_cost: float = WET_COST) -> np.ndarray:
+    """per-cell step cost (include/swe/partition.hpp cost_weights)"""
+    return np.where(np.asarray(state.h) >= h_dry, wet_cost, 1.0)
 
 
 @dataclass
@@ -537,6 +554,6 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 4)
 
 
-__all__ = ["partition", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
+__all__ = ["partition", "cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
            "run_lockstep", "DeviceError"]

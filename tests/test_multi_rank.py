@@ -253,3 +253,19 @@ def test_gloo_link_info_exchange():
         assert cells == [lms[0].n_cells, lms[1].n_cells]
         want = dist.push_plan(lms[r], recv)
         assert all(list(a) == b for a, b in zip(want, plan))
+
+
+@pytest.mark.parametrize("P", [2, 3, 8])
+def test_weighted_partition_balances_work(P):
+    """cost-weighted RCB: every part's weight within one heaviest cell of the
+    target, and a weighted partition is still a valid decomposition"""
+    sc, m = scenario()
+    w = dist.cost_weights(sc.state)
+    part = dist.partition(m, P, w)
+    loads = np.bincount(part, weights=w, minlength=P)
+    assert loads.max() - loads.min() <= 2 * w.max() * np.log2(2 * P)
+    eq = np.bincount(dist.partition(m, P), weights=w, minlength=P)
+    assert loads.max() - loads.min() <= eq.max() - eq.min()
+    lms = [dist.local_mesh(m, part, p) for p in range(P)]
+    owned = np.concatenate([lm.cells[:lm.n_owned] for lm in lms])
+    assert np.array_equal(np.sort(owned), np.arange(m.n_cells))

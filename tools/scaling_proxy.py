@@ -1,0 +1,65 @@
+#!/usr/bin/env python3
+"""Strong-scaling proxy on ONE GPU: split the 10M channel into N RCB parts,
+time each part's step (graph-launched, events) separately, and project the
+N-GPU step as max over parts (+ the measured cost of the linked exchange).
+Prints one JSON line."""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+
+
+def time_part(lp, steps, torch):
+    st = torch.cuda.ExternalStream(lp.lib.swe_dev_stream(lp.ctx))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    H = 1.7976931348623157e308
+    lp.advance(t_end=H, max_steps=5)
+    torch.cuda.synchronize()
+    e0.record(st)
+    lp.launch(t_end=H, max_steps=5 + steps)
+    e1.record(st)
+    torch.cuda.synchronize()
+    lp.records()
+    return e0.elapsed_time(e1) / steps
+
+
+def main():
+    import torch
+    from paper_1807_00672_b200 import api, dist
+    steps = 100
+    sc = api.make_scenario("channel", scale=1.0)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    out = {"cells": mesh.n_cells}
+    one = dist.LinkedPart(dist.local_mesh(mesh, dist.partition(mesh, 1), 0))
+    one.set_state(sc.state)
+    t1 = time_part(one, steps, torch)
+    dist.link_local([one])  # self-linked: the exchange kernel's own cost
+    one.set_state(sc.state)
+    t1l = time_part(one, steps, torch)
+    one.close()
+    out["ms_1"], out["ms_1_linked"] = t1, t1l
+    weights = dist.cost_weights(sc.state) if "--weighted" in sys.argv else None
+    out["partition"] = "cost-weighted RCB" if weights is not None else "equal-count RCB"
+    for n in (2, 4, 8):
+        part = dist.partition(mesh, n, weights)
+        ts, cells, wet = [], [], []
+        for p in range(n):
+            lm = dist.local_mesh(mesh, part, p)
+            lp = dist.LinkedPart(lm)  # unlinked: its own dt; the step cost is what is measured
+            lp.set_state(sc.state)
+            ts.append(time_part(lp, steps, torch))
+            cells.append(lm.n_owned)
+            wet.append(float((sc.state.h[lm.cells[:lm.n_owned]] > 0).mean()))
+            lp.close()
+        mx = max(ts)
+        exch = t1l - t1
+        out[f"N{n}"] = {"ms_parts": ts, "owned_cells": cells, "wet_fraction": wet,
+                        "ms_max": mx, "ms_mean": sum(ts) / n,
+                        "projected_efficiency_no_exchange": t1 / (n * mx),
+                        "projected_efficiency": t1 / (n * (mx + exch))}
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()
