@@ -370,6 +370,7 @@ def run_b200(args):
         _, s_now = solver.clock()
         solver.advance(t_end=horizon, max_steps=s_now + 50)
     _, step0 = solver.clock()
+    skipped0 = solver.info()["skipped_tiles"]
 
     stream = torch.cuda.ExternalStream(solver.stream, device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -385,6 +386,8 @@ def run_b200(args):
     recs = solver.records()
     clk.mark(w0, time.time())
     clk.stop()
+    info0 = solver.info()
+    skip_frac = (info0["skipped_tiles"] - skipped0) / max(1, K * info0["tiles"])
     launches = api.launch_count() - launches0
     assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
     ms = ev0.elapsed_time(ev1)
@@ -396,21 +399,26 @@ def run_b200(args):
     value = world * C * K / (ms / 1e3)
 
     # kernel-level timing: same K steps, plain launches with events per kernel
+    skipped1 = info0["skipped_tiles"]
     solver.set_profiling(True)
     solver.advance_n_async(K, t_end=horizon)
     solver.synchronize()
     kt = solver.kernel_times()
     solver.set_profiling(False)
     info = solver.info()
+    prof_skip = (info["skipped_tiles"] - skipped1) / max(1, K * info["tiles"])
     avg = lambda k: kt[k][0] / max(1, kt[k][1])  # noqa: E731
     fin_ms = avg("finalize")
     peak, peak_src = load_peaks()
     if info["fused"]:
         # k_tile compulsory traffic: cell state/bed/area/n/r in (56 B) + state
         # out (24 B); edge el, er, nx, ny, len, kl, kr (34 B); halo index (4 B)
+        # a dry tile skipped moves 64 B per cell: h, qx, qy, z,
+        # area in, state out -- no edge data
         tile_ms = avg("tile")
         kernels = {"tile": tile_ms, "finalize": fin_ms}
-        dom = ("tile", tile_ms, 80 * C + 34 * E + 4 * info["halo_edges"])
+        full = 80 * C + 34 * E + 4 * info["halo_edges"]
+        dom = ("tile", tile_ms, (1.0 - prof_skip) * full + prof_skip * 64 * C)
     else:
         # k_face_c: edge data 34 B + contributions out 48 B per edge, state+bed
         # gathers 32 B per cell; k_cell_c: 3x3 contributions 72 B + state 24 B
@@ -446,11 +454,21 @@ def run_b200(args):
                         "algorithmic_bytes_per_launch": dom[2],
                         "kernel_ms": kernels,
                         "layout": info,
-                        "step": {"canonical_bytes": "SURVEY.md 8(d) B_step = 116 C + 128 E",
+                        "step": {"canonical_bytes": "SURVEY.md 8(d) B_step = 116 C + 128 E "
+                                                    "(fixed per cell: counts skipped dry tiles "
+                                                    "as full work)",
                                  "algorithmic_bytes": step_bytes,
                                  "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
                                  "frac": step_bytes / (ms / K / 1e3) / 1e9 / peak}},
            "clocks": clk.summary()}
+    if info["fused"]:
+        out["dry_tile_skip"] = {
+            "enabled": bool(info["dry_skip"]), "skipped_tile_fraction": skip_frac,
+            "note": "tiles whose cells and ring were dry and at rest after the previous step "
+                    "are updated without evaluating their edges (every mass flux is exactly "
+                    "+-0, the clamp zeroes q); results bit-identical (tests/test_gpu_parity.py)",
+            "ms_per_step_without_skip": no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch)
+            if info["dry_skip"] else ms / K}
 
     if not args.no_e2e:
         out["e2e"] = e2e_run(api, solver, sc, K, horizon, torch)
@@ -460,6 +478,28 @@ def run_b200(args):
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch):
+    """the same K steps (same starting step) with dry-tile skipping off"""
+    os.environ["SWE_NO_DRY_SKIP"] = "1"
+    try:
+        s = api.DeviceSolver(mesh, device=local)
+    finally:
+        del os.environ["SWE_NO_DRY_SKIP"]
+    s.set_state(sc.state)
+    s.advance(t_end=horizon, max_steps=step0)
+    st = torch.cuda.ExternalStream(s.stream, device=local)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    s.advance_async(t_end=horizon, max_steps=step0 + K)
+    e1.record(st)
+    torch.cuda.synchronize()
+    s.records()
+    ms = e0.elapsed_time(e1) / K
+    s.close()
+    return ms
 
 
 def e2e_run(api, solver, sc, K, horizon, torch):

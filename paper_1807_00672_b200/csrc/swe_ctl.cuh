@@ -52,6 +52,7 @@ struct Ctl {
   unsigned long long xseq;  // exchanges posted so far (linked contexts)
   unsigned int done;        // blocks of the running step kernel that finished
   int tile_next;            // dynamic tile counter of k_tile (reset by finalize)
+  unsigned long long skipped;  // dry tiles skipped by k_tile (cumulative)
 };
 
 struct Part {  // one block's partial results
@@ -130,6 +131,13 @@ struct Dev {
   // tile order, so a tile's slot data is one contiguous range [soff[t], soff[t+1])
   int stage;
   int dyn;  // k_tile fetches tiles from a counter instead of round robin
+  // dry-tile skipping: dryflag[b][t] = every owned cell of tile t is dry and
+  // at rest (0 <= h < h_dry, sign bit clear, q = 0) in state buffer b;
+  // nbr[nbr_off[t] .. nbr_off[t+1]) = tiles holding t's ring cells
+  // (ntiles = a ghost cell of a multi-device part: never skip)
+  int skip;
+  int* dryflag[2];
+  const int *nbr_off, *nbr;
   const int* soff;
   const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
   const double *snx, *sny, *slen;

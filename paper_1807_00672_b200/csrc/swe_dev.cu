@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_select.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -334,6 +335,42 @@ int bits_for(long long v) {
   return b;
 }
 
+// dry-tile skipping: per tile the distinct tiles holding its ring cells
+int build_tile_neighbours(swe_dev_ctx* x) {
+  Dev& d = x->d;
+  cudaStream_t s = x->stream;
+  Temps tmp;
+  const long long np = 2 * ((long long)d.E + x->n_halo);
+  auto* k0 = (unsigned long long*)tmp.get(8 * (size_t)std::max(1LL, np));
+  auto* k1 = (unsigned long long*)tmp.get(8 * (size_t)std::max(1LL, np));
+  auto* k2 = (unsigned long long*)tmp.get(8 * (size_t)std::max(1LL, np));
+  int* nsel = (int*)tmp.get(sizeof(int));
+  if (!k0 || !k1 || !k2 || !nsel) return fail_invalid("dry-skip tables: cudaMalloc failed"), SWE_CUDA;
+  k_tile_pairs<<<blocks_for(32LL * d.ntiles), kBlock, 0, s>>>(d, k0);
+  if (!radix_sort_keys(tmp, k0, k1, (int)np, 32 + bits_for(d.ntiles + 1), s)) return SWE_CUDA;
+  size_t tb = 0;
+  cub::DeviceSelect::Unique(nullptr, tb, k1, k2, nsel, (int)np, s);
+  void* store = tmp.get(tb);
+  if (!store || !cuda_ok(cub::DeviceSelect::Unique(store, tb, k1, k2, nsel, (int)np, s), "unique"))
+    return SWE_CUDA;
+  int nu = 0;
+  CK(cudaMemcpyAsync(&nu, nsel, sizeof(int), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  int* off = x->alloc<int>(d.ntiles + 1);
+  int* nbr = x->alloc<int>(std::max(1, nu));
+  d.dryflag[0] = x->alloc<int>(d.ntiles);
+  d.dryflag[1] = x->alloc<int>(d.ntiles);
+  if (!off || !nbr || !d.dryflag[1]) return fail_invalid("dry-skip tables: cudaMalloc failed"), SWE_CUDA;
+  k_pair_bounds<<<blocks_for(nu), kBlock, 0, s>>>(nu, k2, d.ntiles, off, nbr);
+  CK(cudaMemsetAsync(d.dryflag[0], 0, sizeof(int) * d.ntiles, s));
+  CK(cudaMemsetAsync(d.dryflag[1], 0, sizeof(int) * d.ntiles, s));
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(s));
+  d.nbr_off = off;
+  d.nbr = nbr;
+  return SWE_OK;
+}
+
 int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   Dev& d = x->d;
   const int C = d.C, E = d.E, T = d.T;
@@ -536,6 +573,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   // of 256-cell tiles: the last one 23% busy)
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
+  d.skip = 1;  // dry-tile skipping (fused kernel); SWE_NO_DRY_SKIP=1 turns it off
+  if (const char* env = std::getenv("SWE_NO_DRY_SKIP")) d.skip = std::atoi(env) == 0;
   const int t_max = d.stage ? 128 : 256;  // staged tiles: ~25 KB of shared memory at 128 cells
   int T = t_max;
   if (const char* env = std::getenv("SWE_TILE_CELLS")) {
@@ -619,6 +658,9 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.rec = x->rec;
 
   if (int rc = preprocess(x, m)) return bail(rc);
+  if (!x->fused || d.stage) d.skip = 0;
+  if (d.skip)
+    if (int rc = build_tile_neighbours(x)) return bail(rc);
   if (d.stage) {  // slot arrays of the staged tile kernel
     const size_t ns = (size_t)E + (size_t)x->n_halo;
     int* soff = x->alloc<int>(d.ntiles + 1);
@@ -742,6 +784,10 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
   c.bad_edge = c.bad_cell = c.bad_speed = kNone;
   c.link_err = 0;
   x->cfl_host_valid = false;
+  if (x->d.skip) {  // a new state: no tile is known dry
+    CK(cudaMemsetAsync(x->d.dryflag[0], 0, sizeof(int) * x->d.ntiles, s));
+    CK(cudaMemsetAsync(x->d.dryflag[1], 0, sizeof(int) * x->d.ntiles, s));
+  }
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -1100,10 +1146,12 @@ int swe_dev_kernel_times(swe_dev_ctx* x, double* ms, long long* launches, int n)
 
 int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
   if (!x || !out) return fail_invalid("null argument");
-  const long long v[10] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
+  if (n > 11)
+    if (int rc = sync_ctl(x)) return rc;
+  const long long v[12] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
                            x->grid_tile, x->grid_face, x->grid_cell, (long long)x->tile_smem,
-                           x->d.E};
-  for (int i = 0; i < n && i < 10; ++i) out[i] = v[i];
+                           x->d.E, x->d.skip, n > 11 ? (long long)x->h_ctl->skipped : 0};
+  for (int i = 0; i < n && i < 12; ++i) out[i] = v[i];
   return SWE_OK;
 }
 

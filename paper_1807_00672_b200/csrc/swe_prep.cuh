@@ -153,6 +153,38 @@ __global__ void k_slots(Dev d, int* soff, int* sel, int* ser, int* skk, int* sed
   }
 }
 
+// dry-tile skipping: (tile, neighbour tile) pairs from every slot's two
+// cells; slot j of tile t writes keys[2 (s0 + j) + side] (t << 32 | t when the
+// cell is inside t or a wall)
+__global__ void k_tile_pairs(Dev d, unsigned long long* keys) {
+  const int t = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (t >= d.ntiles) return;
+  const int e0 = d.eoff[t], no = d.eoff[t + 1] - e0;
+  const int h0 = d.hoff[t], ns = no + d.hoff[t + 1] - h0;
+  const int s0 = e0 + h0, c0 = t * d.T, c1 = min(c0 + d.T, d.C_own);
+  for (int j = lane; j < ns; j += 32) {
+    const int e = j < no ? e0 + j : d.halo[h0 + (j - no)];
+    const int cs[2] = {d.el[e], d.er[e]};
+    for (int k = 0; k < 2; ++k) {
+      const int c = cs[k];
+      unsigned long long nb = (unsigned)t;
+      if (c >= 0 && (c < c0 || c >= c1)) nb = c >= d.C_own ? (unsigned)d.ntiles : (unsigned)(c / d.T);
+      keys[2 * (size_t)(s0 + j) + k] = ((unsigned long long)t << 32) | nb;
+    }
+  }
+}
+
+__global__ void k_pair_bounds(int n, const unsigned long long* key, int ntiles, int* off, int* nbr) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const int t = (int)(key[j] >> 32);
+  nbr[j] = (int)(key[j] & 0xffffffffu);
+  const int prev = j == 0 ? -1 : (int)(key[j - 1] >> 32);
+  for (int u = prev + 1; u <= t; ++u) off[u] = j;
+  if (j == n - 1)
+    for (int u = t + 1; u <= ntiles; ++u) off[u] = n;
+}
+
 __global__ void k_fill_int(int n, int* v, int value) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = value;

@@ -259,6 +259,23 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
   return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
 }
 
+// dry-tile skip decision for tile t (warp 0; lane u checks neighbour tile u):
+// the tile and every tile holding its ring cells were dry and at rest after
+// the previous step
+__device__ __forceinline__ int skip_decision(const Dev& d, const int* flags, int t) {
+  int sk = __ldg(flags + t);
+  if (sk) {
+    const int u0 = __ldg(d.nbr_off + t), u1 = __ldg(d.nbr_off + t + 1);
+    int ok = 1;
+    for (int u = u0 + (int)(threadIdx.x & 31); u < u1; u += 32) {
+      const int nb = __ldg(d.nbr + u);
+      ok &= (nb < d.ntiles && __ldg(flags + nb)) ? 1 : 0;
+    }
+    sk = __all_sync(0xffffffffu, ok);
+  }
+  return sk;
+}
+
 // LINK: linked context -- after the update, push the tile's cells that peers
 // hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
 // (Finalizing in the kernel's last block instead of a separate launch was
@@ -287,15 +304,27 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   const Phys P = d.P;
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
-  __shared__ int s_next;
-  for (int t = blockIdx.x; t < d.ntiles;) {
+  __shared__ int s_next, s_skip, s_dec[2];
+  // skip decisions run one tile ahead (static schedule): tile `it`'s decision
+  // is in s_dec[it & 1], made by warp 0 while the previous tile was computed
+  const bool ahead = d.skip && !d.dyn;
+  if (ahead && threadIdx.x < 32 && blockIdx.x < d.ntiles) {
+    const int sk = skip_decision(d, d.dryflag[cur], blockIdx.x);
+    if (threadIdx.x == 0) s_dec[0] = sk;
+  }
+  __syncthreads();
+  int it = 0;
+  for (int t = blockIdx.x; t < d.ntiles; ++it) {
     const int c0 = t * T;
     const int nc = min(T, d.C_own - c0);
-    for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile
+    const bool pre_skip = ahead && s_dec[it & 1] != 0;
+    for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile (a skipped one needs h only)
       sh[i] = H[c0 + i];
-      sq[i] = QX[c0 + i];
-      sr[i] = QY[c0 + i];
-      sz[i] = __ldg(d.z + c0 + i);
+      if (!pre_skip) {
+        sq[i] = QX[c0 + i];
+        sr[i] = QY[c0 + i];
+        sz[i] = __ldg(d.z + c0 + i);
+      }
     }
     const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
     const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
@@ -304,10 +333,31 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
       p0 = __ldg(d.L.tile_push + t);
       p1 = __ldg(d.L.tile_push + t + 1);
     }
+    // dry-tile skip: the tile and its ring were dry and at rest after the
+    // previous step -> every mass flux is exactly +-0, h stays bit-identical,
+    // the dry clamp zeroes q, no CFL contribution
+    if (threadIdx.x < 32) {
+      int sk;
+      if (ahead) {
+        sk = pre_skip;  // decided one tile ahead; now decide the next one
+        const int tn = t + gridDim.x;
+        if (tn < d.ntiles) {
+          const int skn = skip_decision(d, d.dryflag[cur], tn);
+          if (threadIdx.x == 0) s_dec[(it + 1) & 1] = skn;
+        }
+      } else {
+        sk = d.skip ? skip_decision(d, d.dryflag[cur], t) : 0;
+      }
+      if (threadIdx.x == 0) {
+        if (sk) atomicAdd(&ctl->skipped, 1ULL);
+        s_skip = sk;
+      }
+    }
     __syncthreads();
+    const bool skip = s_skip != 0;
 
     // owned + halo edges -> contributions of the in-tile sides
-    for (int j = threadIdx.x; j < ns; j += NT) {
+    for (int j = threadIdx.x; j < (skip ? 0 : ns); j += NT) {
       const int e = j < no ? e0 + j : __ldg(d.halo + h0 + (j - no));
       const int cl = __ldg(d.el + e), cr = __ldg(d.er + e);
       const double nx = __ldg(d.nx + e), ny = __ldg(d.ny + e), len = __ldg(d.len + e);
@@ -352,7 +402,20 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     __syncthreads();
 
     // cell update from the three contribution slots
+    int dry = 1;  // every cell of the tile dry and at rest afterwards
     for (int i = threadIdx.x; i < nc; i += NT) {
+      if (skip) {  // cell_finish of a dry cell with zero mass flux, exactly
+        const double h = sh[i];
+        NH[c0 + i] = h;
+        NQX[c0 + i] = 0.0;
+        NQY[c0 + i] = 0.0;
+        a.mass += h * __ldg(d.area + c0 + i);
+        if (LINK && p1 > p0) {
+          sq[i] = 0.0;
+          sr[i] = 0.0;
+        }
+        continue;
+      }
       double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
 #pragma unroll
       for (int k = 0; k < 3; ++k) {
@@ -361,13 +424,19 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
         ay += ty[3 * i + k];
       }
       const Cons u = cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
+      dry &= (0.0 <= u.h && u.h < P.h_dry) ? 1 : 0;
       if (LINK && p1 > p0) {  // the tile's new state, for the push below
         sh[i] = u.h;
         sq[i] = u.qx;
         sr[i] = u.qy;
       }
     }
-    __syncthreads();
+    if (d.skip) {
+      dry = __syncthreads_and(dry);
+      if (threadIdx.x == 0) d.dryflag[cur ^ 1][t] = dry;
+    } else {
+      __syncthreads();
+    }
     if (LINK && p1 > p0) {
       for (int j = p0 + threadIdx.x; j < p1; j += NT) {
         const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);

@@ -460,3 +460,29 @@ def test_single_wet_cell_spreads_into_dry_cells(coracle):
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(got, k), o[k]), k
     assert np.count_nonzero(got.h) > 50
+
+
+def test_dry_tile_skipping_is_exercised_and_bit_identical(coracle, monkeypatch):
+    """dry-tile skipping: on a mostly dry bed many tiles are
+    skipped, and states, dt and the mass series equal the no-skip run and the
+    oracle bit for bit"""
+    sc = api.make_scenario("sloping_wet_dry", scale=0.04)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    runs = {}
+    for skip in (True, False):
+        if not skip:
+            monkeypatch.setenv("SWE_NO_DRY_SKIP", "1")
+        s = api.DeviceSolver(m)
+        s.set_state(sc.state)
+        recs = s.advance(1e30, max_steps=300)
+        got, _, _ = s.get_state()
+        runs[skip] = (recs, got, s.info())
+    assert runs[True][2]["dry_skip"] == 1 and runs[False][2]["dry_skip"] == 0
+    assert runs[True][2]["skipped_tiles"] > 0.2 * 300 * runs[True][2]["tiles"]
+    assert bit_equal(runs[True][0], runs[False][0])  # dt, max speed AND mass series
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(runs[True][1], k), getattr(runs[False][1], k)), k
+    o = coracle.advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy, nsteps=300)
+    assert bit_equal(runs[True][0][:, 2], o["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(runs[True][1], k), o[k]), k
