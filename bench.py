@@ -236,7 +236,7 @@ def run_b200_dist(args, rank, local, world):
 
     scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
     sc, mesh, setup_s = build_workload(args.config, scale, device=local)
-    part = dist.partition(mesh, world, dist.cost_weights(sc.state))  # equal work per GPU
+    part = dist.partition(mesh, world, dist.cost_weights(sc.state, mesh=mesh))  # equal work
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
     dist.link_torch(lp)
@@ -304,7 +304,8 @@ def run_b200_dist(args, rank, local, world):
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args.config, sc, mesh, 1, {
                    "parallelism": f"{world}-way cost-weighted RCB domain decomposition (wet "
-                                  f"cells weighted {dist.WET_COST}x dry), one part per GPU; "
+                                  f"cells {dist.WET_COST}x, dry cells near water "
+                                  f"{dist.FRONT_COST}x skippable dry ones), one part per GPU; "
                                   "ghost states pushed peer-to-peer by the step kernel, CFL "
                                   "bound / outcome through device mailboxes (no host round "
                                   "trip per step)",
@@ -413,12 +414,12 @@ def run_b200(args):
     if info["fused"]:
         # k_tile compulsory traffic: cell state/bed/area/n/r in (56 B) + state
         # out (24 B); edge el, er, nx, ny, len, kl, kr (34 B); halo index (4 B)
-        # a dry tile skipped moves 64 B per cell: h, qx, qy, z,
-        # area in, state out -- no edge data
+        # a dry tile skipped moves 40 B per cell: h and area in,
+        # state out -- no edge data, no qx / qy / bed
         tile_ms = avg("tile")
         kernels = {"tile": tile_ms, "finalize": fin_ms}
         full = 80 * C + 34 * E + 4 * info["halo_edges"]
-        dom = ("tile", tile_ms, (1.0 - prof_skip) * full + prof_skip * 64 * C)
+        dom = ("tile", tile_ms, (1.0 - prof_skip) * full + prof_skip * 40 * C)
     else:
         # k_face_c: edge data 34 B + contributions out 48 B per edge, state+bed
         # gathers 32 B per cell; k_cell_c: 3x3 contributions 72 B + state 24 B

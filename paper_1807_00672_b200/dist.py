@@ -54,12 +54,32 @@ def partition(mesh: Mesh, nparts: int, weights=None) -> np.ndarray:
     return out
 
 
-WET_COST = 1.65  # wet / dry cell step cost on B200 (tools/scaling_proxy.py)
+WET_COST = 3.5    # wet / skipped-dry cell step cost on B200 (tools/scaling_proxy.py)
+FRONT_COST = 2.1  # dry cells near water: their tiles are computed, not skipped
+FRONT_WIDTH = 8   # cells: about half a tile's extent
 
 
-def cost_weights(state: FieldState, h_dry: float = 1e-6, wet_cost: float = WET_COST) -> np.ndarray:
-    """per-cell step cost (include/swe/partition.hpp cost_weights)"""
-    return np.where(np.asarray(state.h) >= h_dry, wet_cost, 1.0)
+def cost_weights(state: FieldState, h_dry: float = 1e-6, wet_cost: float = WET_COST,
+                 mesh: Mesh | None = None, front_cost: float = FRONT_COST,
+                 front_width: int = FRONT_WIDTH) -> np.ndarray:
+    """per-cell step cost (include/swe/partition.hpp cost_weights): 1 for a
+    dry cell in a skippable dry region, wet_cost for a wet one; with `mesh`,
+    dry cells within front_width cells of water cost front_cost (dry-tile
+    skipping needs the tile AND its ring dry)."""
+    wet = np.asarray(state.h) >= h_dry
+    w = np.where(wet, wet_cost, 1.0)
+    if mesh is not None and front_width > 0:
+        el, er = np.asarray(mesh.edge_left), np.asarray(mesh.edge_right)
+        inner = er >= 0
+        a, b = el[inner], er[inner]
+        near = wet.copy()
+        for _ in range(front_width):  # dilate the wet set across edges
+            grow = near.copy()
+            grow[a] |= near[b]
+            grow[b] |= near[a]
+            near = grow
+        w = np.where(~wet & near, front_cost, w)
+    return w
 
 
 @dataclass

@@ -39,7 +39,7 @@ def main():
     t1l = time_part(one, steps, torch)
     one.close()
     out["ms_1"], out["ms_1_linked"] = t1, t1l
-    weights = dist.cost_weights(sc.state) if "--weighted" in sys.argv else None
+    weights = dist.cost_weights(sc.state, mesh=mesh) if "--weighted" in sys.argv else None
     out["partition"] = "cost-weighted RCB" if weights is not None else "equal-count RCB"
     for n in (2, 4, 8):
         part = dist.partition(mesh, n, weights)
