@@ -318,6 +318,27 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     const int c0 = t * T;
     const int nc = min(T, d.C_own - c0);
     const bool pre_skip = ahead && s_dec[it & 1] != 0;
+    if (!LINK && pre_skip) {  // skipped tile, fast path: no shared memory, one round trip
+      if (threadIdx.x < 32) {
+        const int tn = t + gridDim.x;
+        const int skn = tn < d.ntiles ? skip_decision(d, d.dryflag[cur], tn) : 0;
+        if (threadIdx.x == 0) {
+          s_dec[(it + 1) & 1] = skn;
+          d.dryflag[cur ^ 1][t] = 1;
+          atomicAdd(&ctl->skipped, 1ULL);
+        }
+      }
+      for (int i = threadIdx.x; i < nc; i += NT) {
+        const double h = H[c0 + i];
+        NH[c0 + i] = h;
+        NQX[c0 + i] = 0.0;
+        NQY[c0 + i] = 0.0;
+        a.mass += h * __ldg(d.area + c0 + i);
+      }
+      __syncthreads();  // s_dec of the next tile
+      t += gridDim.x;
+      continue;
+    }
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile (a skipped one needs h only)
       sh[i] = H[c0 + i];
       if (!pre_skip) {
