@@ -131,12 +131,14 @@ struct Dev {
   // tile order, so a tile's slot data is one contiguous range [soff[t], soff[t+1])
   int stage;
   int dyn;  // k_tile fetches tiles from a counter instead of round robin
-  // dry-tile skipping: dryflag[b][t] = every owned cell of tile t is dry and
-  // at rest (0 <= h < h_dry, sign bit clear, q = 0) in state buffer b;
-  // nbr[nbr_off[t] .. nbr_off[t+1]) = tiles holding t's ring cells
-  // (ntiles = a ghost cell of a multi-device part: never skip)
+  // dry-tile skipping: dryflag[t] = tag of the state (step + 1) in which every
+  // owned cell of tile t is dry and at rest (0 <= h < h_dry, q = 0), else 0;
+  // skipmask[t] = that tag when tile t AND every tile holding its ring cells
+  // carry it (nbr[nbr_off[t] .. nbr_off[t+1]); ntiles = a ghost cell of a
+  // multi-device part: never skip)
   int skip;
-  int* dryflag[2];
+  int* dryflag;
+  int* skipmask;
   const int *nbr_off, *nbr;
   const int* soff;
   const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
@@ -552,9 +554,31 @@ __device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHand
   finalize_step(d, g, status, status == SWE_NEGATIVE_DEPTH ? neg : blow, err_h, cond, use_cond);
 }
 
+// skip mask of tile u for the next step (blocks >= 1 of the finalize /
+// exchange / post launch, one thread per tile; reads the flags k_tile wrote)
+__device__ __forceinline__ bool skip_mask_blocks(const Dev& d) {
+  if (blockIdx.x == 0) return false;
+  const int u = (blockIdx.x - 1) * blockDim.x + threadIdx.x;
+  if (d.skip && u < d.ntiles) {
+    const int f = d.dryflag[u];
+    const int v0 = d.nbr_off[u], v1 = d.nbr_off[u + 1];
+    int ok = f != 0;
+    // no early exit: the neighbour loads are independent and issue together
+#pragma unroll 4
+    for (int v = v0; v < v1; ++v) {
+      const int nb = d.nbr[v];
+      const int fl = nb < d.ntiles ? d.dryflag[nb] : 0;
+      ok &= fl == f ? 1 : 0;
+    }
+    d.skipmask[u] = ok ? f : 0;
+  }
+  return true;
+}
+
 // kernel forms
 __global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphConditionalHandle cond,
                                                      int use_cond) {
+  if (skip_mask_blocks(d)) return;
   if (!d.ctl->active) {
     if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
     return;
@@ -564,6 +588,7 @@ __global__ void __launch_bounds__(kBlock) k_finalize(Dev d, int n, cudaGraphCond
 }
 
 __global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
+  if (skip_mask_blocks(d)) return;
   if (kind == 0 && !d.ctl->active) return;
   const Part p = reduce_parts(d, n);
   if (threadIdx.x < 32) post_outcome(d, p, kind);
@@ -572,6 +597,7 @@ __global__ void __launch_bounds__(kBlock) k_post(Dev d, int n, int kind) {
 // post + wait in one launch (the graph / plain path of a linked context)
 __global__ void __launch_bounds__(kBlock) k_exchange(Dev d, int n, int kind,
                                                      cudaGraphConditionalHandle cond, int use_cond) {
+  if (skip_mask_blocks(d)) return;
   if (kind == 0 && !d.ctl->active) {
     if (threadIdx.x == 0 && use_cond) cudaGraphSetConditional(cond, 0);
     return;

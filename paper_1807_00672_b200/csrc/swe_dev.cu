@@ -171,8 +171,11 @@ int launch_update(swe_dev_ctx* x) {
 }
 
 // linked: post this rank's outcome / CFL bound, then wait for every rank's
+// extra blocks of the launch after the step kernel: the next step's skip mask
+int mask_blocks(const swe_dev_ctx* x) { return x->d.skip ? blocks_for(x->d.ntiles) : 0; }
+
 int launch_post(swe_dev_ctx* x, int n, int kind) {
-  k_post<<<1, kBlock, 0, x->stream>>>(x->d, n, kind);
+  k_post<<<1 + (kind == 0 ? mask_blocks(x) : 0), kBlock, 0, x->stream>>>(x->d, n, kind);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_post") ? SWE_OK : SWE_CUDA;
 }
@@ -184,14 +187,15 @@ int launch_wait(swe_dev_ctx* x, int kind, cudaGraphConditionalHandle h, int use_
 }
 
 int launch_exchange(swe_dev_ctx* x, int n, int kind, cudaGraphConditionalHandle h, int use_cond) {
-  k_exchange<<<1, kBlock, 0, x->stream>>>(x->d, n, kind, h, use_cond);
+  k_exchange<<<1 + (kind == 0 ? mask_blocks(x) : 0), kBlock, 0, x->stream>>>(x->d, n, kind, h,
+                                                                            use_cond);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_exchange") ? SWE_OK : SWE_CUDA;
 }
 
 int launch_finalize(swe_dev_ctx* x, cudaGraphConditionalHandle h, int use_cond) {
   if (x->linked) return launch_exchange(x, x->n_step_parts(), 0, h, use_cond);
-  k_finalize<<<1, kBlock, 0, x->stream>>>(x->d, x->n_step_parts(), h, use_cond);
+  k_finalize<<<1 + mask_blocks(x), kBlock, 0, x->stream>>>(x->d, x->n_step_parts(), h, use_cond);
   ++g_launches;
   return cuda_ok(cudaGetLastError(), "k_finalize") ? SWE_OK : SWE_CUDA;
 }
@@ -358,12 +362,12 @@ int build_tile_neighbours(swe_dev_ctx* x) {
   CK(cudaStreamSynchronize(s));
   int* off = x->alloc<int>(d.ntiles + 1);
   int* nbr = x->alloc<int>(std::max(1, nu));
-  d.dryflag[0] = x->alloc<int>(d.ntiles);
-  d.dryflag[1] = x->alloc<int>(d.ntiles);
-  if (!off || !nbr || !d.dryflag[1]) return fail_invalid("dry-skip tables: cudaMalloc failed"), SWE_CUDA;
+  d.dryflag = x->alloc<int>(d.ntiles);
+  d.skipmask = x->alloc<int>(d.ntiles);
+  if (!off || !nbr || !d.skipmask) return fail_invalid("dry-skip tables: cudaMalloc failed"), SWE_CUDA;
   k_pair_bounds<<<blocks_for(nu), kBlock, 0, s>>>(nu, k2, d.ntiles, off, nbr);
-  CK(cudaMemsetAsync(d.dryflag[0], 0, sizeof(int) * d.ntiles, s));
-  CK(cudaMemsetAsync(d.dryflag[1], 0, sizeof(int) * d.ntiles, s));
+  CK(cudaMemsetAsync(d.dryflag, 0, sizeof(int) * d.ntiles, s));
+  CK(cudaMemsetAsync(d.skipmask, 0, sizeof(int) * d.ntiles, s));
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(s));
   d.nbr_off = off;
@@ -785,8 +789,8 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
   c.link_err = 0;
   x->cfl_host_valid = false;
   if (x->d.skip) {  // a new state: no tile is known dry
-    CK(cudaMemsetAsync(x->d.dryflag[0], 0, sizeof(int) * x->d.ntiles, s));
-    CK(cudaMemsetAsync(x->d.dryflag[1], 0, sizeof(int) * x->d.ntiles, s));
+    CK(cudaMemsetAsync(x->d.dryflag, 0, sizeof(int) * x->d.ntiles, s));
+    CK(cudaMemsetAsync(x->d.skipmask, 0, sizeof(int) * x->d.ntiles, s));
   }
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));

@@ -259,23 +259,6 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
   return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
 }
 
-// dry-tile skip decision for tile t (warp 0; lane u checks neighbour tile u):
-// the tile and every tile holding its ring cells were dry and at rest after
-// the previous step
-__device__ __forceinline__ int skip_decision(const Dev& d, const int* flags, int t) {
-  int sk = __ldg(flags + t);
-  if (sk) {
-    const int u0 = __ldg(d.nbr_off + t), u1 = __ldg(d.nbr_off + t + 1);
-    int ok = 1;
-    for (int u = u0 + (int)(threadIdx.x & 31); u < u1; u += 32) {
-      const int nb = __ldg(d.nbr + u);
-      ok &= (nb < d.ntiles && __ldg(flags + nb)) ? 1 : 0;
-    }
-    sk = __all_sync(0xffffffffu, ok);
-  }
-  return sk;
-}
-
 // LINK: linked context -- after the update, push the tile's cells that peers
 // hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
 // (Finalizing in the kernel's last block instead of a separate launch was
@@ -305,13 +288,14 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
   __shared__ int s_next, s_skip, s_dec[2];
-  // skip decisions run one tile ahead (static schedule): tile `it`'s decision
-  // is in s_dec[it & 1], made by warp 0 while the previous tile was computed
+  // dry-tile skipping: skipmask[t] == tag(state) <=> tile t and its ring were
+  // dry and at rest (computed by the finalize launch from the flags this
+  // kernel writes, tagged with the step of the state they describe).
+  // Decisions are read one tile ahead (static schedule): s_dec[it & 1].
+  const int tag = (int)(ctl->step + 1);
   const bool ahead = d.skip && !d.dyn;
-  if (ahead && threadIdx.x < 32 && blockIdx.x < d.ntiles) {
-    const int sk = skip_decision(d, d.dryflag[cur], blockIdx.x);
-    if (threadIdx.x == 0) s_dec[0] = sk;
-  }
+  if (ahead && threadIdx.x == 0)
+    s_dec[0] = blockIdx.x < d.ntiles && __ldg(d.skipmask + blockIdx.x) == tag;
   __syncthreads();
   int it = 0;
   for (int t = blockIdx.x; t < d.ntiles; ++it) {
@@ -319,14 +303,11 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     const int nc = min(T, d.C_own - c0);
     const bool pre_skip = ahead && s_dec[it & 1] != 0;
     if (!LINK && pre_skip) {  // skipped tile, fast path: no shared memory, one round trip
-      if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) {
         const int tn = t + gridDim.x;
-        const int skn = tn < d.ntiles ? skip_decision(d, d.dryflag[cur], tn) : 0;
-        if (threadIdx.x == 0) {
-          s_dec[(it + 1) & 1] = skn;
-          d.dryflag[cur ^ 1][t] = 1;
-          atomicAdd(&ctl->skipped, 1ULL);
-        }
+        s_dec[(it + 1) & 1] = tn < d.ntiles && __ldg(d.skipmask + tn) == tag;
+        d.dryflag[t] = tag + 1;
+        atomicAdd(&ctl->skipped, 1ULL);
       }
       for (int i = threadIdx.x; i < nc; i += NT) {
         const double h = H[c0 + i];
@@ -357,22 +338,17 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     // dry-tile skip: the tile and its ring were dry and at rest after the
     // previous step -> every mass flux is exactly +-0, h stays bit-identical,
     // the dry clamp zeroes q, no CFL contribution
-    if (threadIdx.x < 32) {
+    if (threadIdx.x == 0) {
       int sk;
       if (ahead) {
-        sk = pre_skip;  // decided one tile ahead; now decide the next one
+        sk = pre_skip;  // decided one tile ahead; now read the next decision
         const int tn = t + gridDim.x;
-        if (tn < d.ntiles) {
-          const int skn = skip_decision(d, d.dryflag[cur], tn);
-          if (threadIdx.x == 0) s_dec[(it + 1) & 1] = skn;
-        }
+        s_dec[(it + 1) & 1] = tn < d.ntiles && __ldg(d.skipmask + tn) == tag;
       } else {
-        sk = d.skip ? skip_decision(d, d.dryflag[cur], t) : 0;
+        sk = d.skip && __ldg(d.skipmask + t) == tag;
       }
-      if (threadIdx.x == 0) {
-        if (sk) atomicAdd(&ctl->skipped, 1ULL);
-        s_skip = sk;
-      }
+      if (sk) atomicAdd(&ctl->skipped, 1ULL);
+      s_skip = sk;
     }
     __syncthreads();
     const bool skip = s_skip != 0;
@@ -454,7 +430,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     }
     if (d.skip) {
       dry = __syncthreads_and(dry);
-      if (threadIdx.x == 0) d.dryflag[cur ^ 1][t] = dry;
+      if (threadIdx.x == 0) d.dryflag[t] = dry ? tag + 1 : 0;  // describes the next state
     } else {
       __syncthreads();
     }

@@ -71,6 +71,10 @@ def main():
     s.synchronize()
     kt = s.kernel_times()
     out["kernel_ms"] = {k: v[0] / max(1, v[1]) for k, v in kt.items()}
+    inf = s.info()
+    if "skipped_tiles" in inf:
+        _, steps_done = s.clock()
+        out["skipped_per_step"] = inf["skipped_tiles"] / max(1, steps_done) / max(1, inf["tiles"])
     print(json.dumps(out))
 
 
