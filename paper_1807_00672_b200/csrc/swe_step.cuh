@@ -287,37 +287,53 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   const Phys P = d.P;
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
-  __shared__ int s_next, s_skip, s_dec[2];
+  constexpr int kAhead = 4;  // skip decisions known ahead per CTA (ring s_dec[8])
+  __shared__ int s_next, s_skip, s_dec[8];
   // dry-tile skipping: skipmask[t] == tag(state) <=> tile t and its ring were
   // dry and at rest (computed by the finalize launch from the flags this
-  // kernel writes, tagged with the step of the state they describe).
-  // Decisions are read one tile ahead (static schedule): s_dec[it & 1].
+  // kernel writes, tagged with the step of the state they describe).  With
+  // the static schedule the decisions of this CTA's next kAhead tiles sit in
+  // s_dec[it .. it + kAhead) (mod 8), refilled by thread 0.
   const int tag = (int)(ctl->step + 1);
   const bool ahead = d.skip && !d.dyn;
   if (ahead && threadIdx.x == 0)
-    s_dec[0] = blockIdx.x < d.ntiles && __ldg(d.skipmask + blockIdx.x) == tag;
+    for (int k = 0; k < kAhead; ++k) {
+      const int tk = blockIdx.x + k * gridDim.x;
+      s_dec[k] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
+    }
   __syncthreads();
   int it = 0;
-  for (int t = blockIdx.x; t < d.ntiles; ++it) {
+  for (int t = blockIdx.x; t < d.ntiles;) {
     const int c0 = t * T;
     const int nc = min(T, d.C_own - c0);
-    const bool pre_skip = ahead && s_dec[it & 1] != 0;
-    if (!LINK && pre_skip) {  // skipped tile, fast path: no shared memory, one round trip
+    const bool pre_skip = ahead && s_dec[it & 7] != 0;
+    if (!LINK && pre_skip) {
+      // skipped tiles, fast path: a run of up to kAhead consecutive skipped
+      // tiles of this CTA in one round trip, no shared memory
+      int run = 1;
+      while (run < kAhead && s_dec[(it + run) & 7]) ++run;
       if (threadIdx.x == 0) {
-        const int tn = t + gridDim.x;
-        s_dec[(it + 1) & 1] = tn < d.ntiles && __ldg(d.skipmask + tn) == tag;
-        d.dryflag[t] = tag + 1;
-        atomicAdd(&ctl->skipped, 1ULL);
+        for (int k = 0; k < run; ++k) {
+          const int tk = t + (kAhead + k) * gridDim.x;
+          s_dec[(it + kAhead + k) & 7] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
+          d.dryflag[t + k * gridDim.x] = tag + 1;
+        }
+        atomicAdd(&ctl->skipped, (unsigned long long)run);
       }
-      for (int i = threadIdx.x; i < nc; i += NT) {
-        const double h = H[c0 + i];
-        NH[c0 + i] = h;
-        NQX[c0 + i] = 0.0;
-        NQY[c0 + i] = 0.0;
-        a.mass += h * __ldg(d.area + c0 + i);
+      for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
+        const int ck = (t + k * gridDim.x) * T;
+        const int nk = min(T, d.C_own - ck);
+        for (int i = threadIdx.x; i < nk; i += NT) {
+          const double h = H[ck + i];
+          NH[ck + i] = h;
+          NQX[ck + i] = 0.0;
+          NQY[ck + i] = 0.0;
+          a.mass += h * __ldg(d.area + ck + i);
+        }
       }
-      __syncthreads();  // s_dec of the next tile
-      t += gridDim.x;
+      __syncthreads();  // s_dec refill
+      t += run * gridDim.x;
+      it += run;
       continue;
     }
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile (a skipped one needs h only)
@@ -341,9 +357,9 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     if (threadIdx.x == 0) {
       int sk;
       if (ahead) {
-        sk = pre_skip;  // decided one tile ahead; now read the next decision
-        const int tn = t + gridDim.x;
-        s_dec[(it + 1) & 1] = tn < d.ntiles && __ldg(d.skipmask + tn) == tag;
+        sk = pre_skip;  // decided ahead; refill the ring
+        const int tk = t + kAhead * gridDim.x;
+        s_dec[(it + kAhead) & 7] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
       } else {
         sk = d.skip && __ldg(d.skipmask + t) == tag;
       }
@@ -452,6 +468,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
     } else {
       t += gridDim.x;
     }
+    ++it;
   }
   block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + blockIdx.x);
 }
