@@ -236,7 +236,8 @@ def run_b200_dist(args, rank, local, world):
 
     scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
     sc, mesh, setup_s = build_workload(args.config, scale, device=local)
-    part = dist.partition(mesh, world, dist.cost_weights(sc.state, mesh=mesh))  # equal work
+    # equal work per GPU: cells weighted by the device's own dry-tile skip pattern
+    part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local))
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
     dist.link_torch(lp)
@@ -303,9 +304,9 @@ def run_b200_dist(args, rank, local, world):
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args.config, sc, mesh, 1, {
-                   "parallelism": f"{world}-way cost-weighted RCB domain decomposition (wet "
-                                  f"cells {dist.WET_COST}x, dry cells near water "
-                                  f"{dist.FRONT_COST}x skippable dry ones), one part per GPU; "
+                   "parallelism": f"{world}-way cost-weighted RCB domain decomposition (cells "
+                                  f"of computed tiles {dist.COMPUTED_COST}x cells of skipped dry "
+                                  "tiles, measured on the device), one part per GPU; "
                                   "ghost states pushed peer-to-peer by the step kernel, CFL "
                                   "bound / outcome through device mailboxes (no host round "
                                   "trip per step)",

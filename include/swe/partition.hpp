@@ -28,7 +28,7 @@ namespace swe {
 /// median (equal cell counts); with per-cell weights (the step's cost per
 /// cell, see cost_weights) it is the weighted median, so parts get equal
 /// WORK -- on a partly dry domain equal counts leave the wet parts slower
-/// (measured: a dry 1.28M-cell part steps in 0.035 ms, a wet one in 0.117).
+/// (measured: a dry 1.28M-cell part steps in 0.027 ms, a wet one in 0.115).
 inline std::vector<int> rcb_partition(const Mesh& m, int nparts,
                                       const std::vector<double>* weights = nullptr) {
   if (nparts < 1) throw config_error("rcb_partition: nparts must be >= 1");
@@ -84,11 +84,12 @@ inline std::vector<int> rcb_partition(const Mesh& m, int nparts,
 }
 
 /// Per-cell cost of the fused step for a weighted partition: 1 for a dry
-/// cell, wet_cost for a wet one (h >= h_dry).  wet_cost = 3.5 fits the
-/// measured part step times on B200 with dry-tile skipping (a dry 1.28M-cell
-/// part 0.035 ms, a wet one 0.117 ms, tools/scaling_proxy.py).
+/// cell, wet_cost for a wet one (h >= h_dry).  wet_cost = 5 fits the
+/// measured part step times on B200 with dry-tile skipping (least squares
+/// over 2/4/8-part splits of the 10M channel: 0.080 ms per million wet
+/// cells, 0.015 per million dry ones, tools/scaling_proxy.py).
 inline std::vector<double> cost_weights(const std::vector<double>& h, double h_dry,
-                                        double wet_cost = 3.5) {
+                                        double wet_cost = 5.0) {
   std::vector<double> w(h.size());
   for (size_t c = 0; c < h.size(); ++c) w[c] = h[c] >= h_dry ? wet_cost : 1.0;
   return w;

@@ -232,6 +232,11 @@ SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launch
  * [11] dry tiles skipped so far (n > 11 synchronises the context). */
 SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
 
+/* Per cell (reference numbering): 1 if dry-tile skipping will skip the cell's
+ * tile in the next step (the measured cost pattern behind cost-weighted
+ * partitions, paper_1807_00672_b200/dist.py measured_cost_weights). */
+SWE_API int swe_dev_cell_skip(swe_dev_ctx* ctx, unsigned char* skipped);
+
 /* cudaStream_t of the context (as void*), for events on the launching stream. */
 SWE_API void* swe_dev_stream(swe_dev_ctx* ctx);
 /* Device bytes held by the context. */

@@ -567,6 +567,12 @@ class DeviceSolver:
         _status(rc, st, "swe_dev_records")
         return out
 
+    def cell_skip(self) -> np.ndarray:
+        """per cell: 1 if its tile is skipped (dry) in the next step"""
+        out = np.empty(self.n_cells, np.uint8)
+        _check(self.lib.swe_dev_cell_skip(self.ctx, L.ptr(out)), "swe_dev_cell_skip")
+        return out
+
     def advance_n_async(self, n: int, t_end: float = float("inf")):
         _check(self.lib.swe_dev_advance_n_async(self.ctx, n, t_end), "swe_dev_advance_n_async")
 

@@ -1630,6 +1630,25 @@ int swe_dev_built_export(swe_built_mesh* b, int* cell_nodes, double* area, doubl
 
 void swe_dev_built_free(swe_built_mesh* b) { delete b; }
 
+int swe_dev_cell_skip(swe_dev_ctx* x, unsigned char* skipped) {
+  if (!x || !skipped) return fail_invalid("swe_dev_cell_skip: null argument");
+  const int C = x->d.C;
+  if (int rc = sync_ctl(x)) return rc;
+  unsigned char* dv = nullptr;
+  CK(cudaMalloc(&dv, (size_t)C));
+  if (x->d.skip) {
+    k_cell_skip<<<blocks_for(C), kBlock, 0, x->stream>>>(x->d, (int)(x->h_ctl->step + 1), dv);
+    ++g_launches;
+  } else {
+    CK(cudaMemsetAsync(dv, 0, (size_t)C, x->stream));
+  }
+  CK(cudaGetLastError());
+  CK(cudaMemcpyAsync(skipped, dv, (size_t)C, cudaMemcpyDeviceToHost, x->stream));
+  CK(cudaStreamSynchronize(x->stream));
+  cudaFree(dv);
+  return SWE_OK;
+}
+
 void* swe_dev_stream(swe_dev_ctx* x) { return x ? (void*)x->stream : nullptr; }
 
 long long swe_dev_memory_bytes(swe_dev_ctx* x) { return x ? x->bytes : 0; }

@@ -185,6 +185,14 @@ __global__ void k_pair_bounds(int n, const unsigned long long* key, int ntiles, 
     for (int u = t + 1; u <= ntiles; ++u) off[u] = n;
 }
 
+// per reference cell: 1 if its tile is skipped in the next step (dry-tile
+// skipping), for cost-weighted partitions
+__global__ void k_cell_skip(Dev d, int tag, unsigned char* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d.C) return;
+  out[d.c_orig[c]] = (c < d.C_own && d.skipmask[c / d.T] == tag) ? 1 : 0;
+}
+
 __global__ void k_fill_int(int n, int* v, int value) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) v[i] = value;

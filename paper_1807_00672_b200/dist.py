@@ -54,8 +54,8 @@ def partition(mesh: Mesh, nparts: int, weights=None) -> np.ndarray:
     return out
 
 
-WET_COST = 3.5    # wet / skipped-dry cell step cost on B200 (tools/scaling_proxy.py)
-FRONT_COST = 2.1  # dry cells near water: their tiles are computed, not skipped
+WET_COST = 5.0    # wet / skipped-dry cell step cost on B200 (tools/scaling_proxy.py fit)
+FRONT_COST = 3.0  # dry cells near water: their tiles are computed, not skipped
 FRONT_WIDTH = 8   # cells: about half a tile's extent
 
 
@@ -80,6 +80,24 @@ def cost_weights(state: FieldState, h_dry: float = 1e-6, wet_cost: float = WET_C
             near = grow
         w = np.where(~wet & near, front_cost, w)
     return w
+
+
+COMPUTED_COST = 3.8  # computed / skipped tile cost per cell (calibrated on 2/4/8-part splits)
+
+
+def measured_cost_weights(mesh: Mesh, state: FieldState, device: int = 0, steps: int = 2,
+                          computed_cost: float = COMPUTED_COST) -> np.ndarray:
+    """per-cell cost from the device's own skip pattern: run the whole mesh
+    `steps` steps and weight cells in skipped dry tiles 1, all others
+    computed_cost (captures the wet front at tile granularity)"""
+    from .api import DeviceSolver
+    s = DeviceSolver(mesh, device=device)
+    try:
+        s.set_state(state)
+        s.advance(1.7976931348623157e308, max_steps=steps)
+        return np.where(s.cell_skip() != 0, 1.0, computed_cost)
+    finally:
+        s.close()
 
 
 @dataclass
@@ -574,6 +592,6 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 4)
 
 
-__all__ = ["partition", "cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
+__all__ = ["partition", "cost_weights", "measured_cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
            "run_lockstep", "DeviceError"]

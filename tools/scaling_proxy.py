@@ -39,8 +39,16 @@ def main():
     t1l = time_part(one, steps, torch)
     one.close()
     out["ms_1"], out["ms_1_linked"] = t1, t1l
-    weights = dist.cost_weights(sc.state, mesh=mesh) if "--weighted" in sys.argv else None
-    out["partition"] = "cost-weighted RCB" if weights is not None else "equal-count RCB"
+    weights = None
+    out["partition"] = "equal-count RCB"
+    if "--weighted" in sys.argv:
+        weights = dist.cost_weights(sc.state, mesh=mesh)
+        out["partition"] = "cost-weighted RCB (wet/dry model)"
+    if "--measured" in sys.argv:
+        cc = float(sys.argv[sys.argv.index("--measured") + 1]) \
+            if len(sys.argv) > sys.argv.index("--measured") + 1 else dist.COMPUTED_COST
+        weights = dist.measured_cost_weights(mesh, sc.state, computed_cost=cc)
+        out["partition"] = f"cost-weighted RCB (measured skip pattern, computed tiles {cc}x)"
     for n in (2, 4, 8):
         part = dist.partition(mesh, n, weights)
         ts, cells, wet = [], [], []
