@@ -271,6 +271,7 @@ def run_b200_dist(args, rank, local, world):
             break
         steps += 50
         advance(steps)
+    skipped0 = lp_skipped(lp)
     stream = torch.cuda.ExternalStream(dist_stream(lp), device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tdist.barrier()
@@ -288,6 +289,10 @@ def run_b200_dist(args, rank, local, world):
     assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
     ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
+    # dry tiles skipped over the timed steps, summed over ranks
+    sk = torch.tensor([float(lp_skipped(lp) - skipped0), float(lp_tiles(lp) * K)], device=dev)
+    tdist.all_reduce(sk, op=tdist.ReduceOp.SUM)
+    skip_frac = float(sk[0].item()) / max(1.0, float(sk[1].item()))
     ms = float(ms.item())
     C = mesh.n_cells
     # e2e: host state in, K steps, owned state back to the host
@@ -318,6 +323,7 @@ def run_b200_dist(args, rank, local, world):
                                     "K x (k_tile with halo push, k_exchange) in a conditional "
                                     "WHILE node",
                "clocks": clk.summary() if clk else None,
+               "roofline": dist_roofline(mesh, K, ms, world, skip_frac),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
                        "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": (24 * C + 40 * K) / K,
                        "path": "LinkedPart.set_state (host) + advance (K steps, records D2H) + "
@@ -330,6 +336,35 @@ def run_b200_dist(args, rank, local, world):
     tdist.barrier()
     lp.close()
     tdist.destroy_process_group()
+
+
+def _lp_info(lp):
+    import ctypes
+    v = (ctypes.c_longlong * 12)()
+    lp.lib.swe_dev_info(lp.ctx, v, 12)
+    return list(v)
+
+
+def lp_skipped(lp):
+    return _lp_info(lp)[11]
+
+
+def lp_tiles(lp):
+    return _lp_info(lp)[2]
+
+
+def dist_roofline(mesh, K, ms, world, skip_frac):
+    """whole-job step roofline of an N-GPU run: SURVEY §8(d) canonical step
+    bytes (skipped dry tiles at 40 B/cell) over the max-over-ranks step time,
+    against N x the per-GPU HBM peak"""
+    peak, src = load_peaks()
+    C, E = mesh.n_cells, mesh.n_edges
+    step = (1.0 - skip_frac) * (116 * C + 128 * E) + skip_frac * 40 * C
+    achieved = step / (ms / K / 1e3) / 1e9
+    return {"bound": "hbm", "kernel": "step (all ranks)", "achieved": achieved,
+            "peak": world * peak, "unit": "GB/s", "frac": achieved / (world * peak),
+            "traffic": None, "peak_source": f"{world} x {src}",
+            "skipped_tile_fraction": skip_frac}
 
 
 def dist_stream(part_solver):
