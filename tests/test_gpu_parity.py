@@ -486,3 +486,28 @@ def test_dry_tile_skipping_is_exercised_and_bit_identical(coracle, monkeypatch):
     assert bit_equal(runs[True][0][:, 2], o["dts"])
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(runs[True][1], k), o[k]), k
+
+
+@pytest.mark.parametrize("config,scale,steps", [("three_mounds_friction", 1.0, 3000),
+                                                ("sloping_wet_dry", 0.3, 3000)])
+def test_dry_skip_long_runs_equal_no_skip(monkeypatch, config, scale, steps):
+    """~1M cells, thousands of steps while fronts sweep over dry tiles: the
+    skipping run equals the full evaluation bit for bit (state, dt, speed,
+    mass series, clip ledger)"""
+    sc = api.make_scenario(config, scale=scale)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    out = []
+    for off in ("0", "1"):
+        monkeypatch.setenv("SWE_NO_DRY_SKIP", off)
+        s = api.DeviceSolver(m)
+        s.set_state(sc.state)
+        recs = s.advance(1e30, max_steps=steps)
+        st, t, n = s.get_state()
+        out.append((recs, st, t, n, s.ledger(), s.info()))
+        s.close()
+    (ra, sa, ta, na, la, ia), (rb, sb, tb, nb, lb, ib) = out
+    assert ia["dry_skip"] == 1 and ib["dry_skip"] == 0 and ia["skipped_tiles"] > 0
+    assert na == nb == steps and ta == tb and la == lb
+    assert bit_equal(ra, rb)
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(sa, k), getattr(sb, k)), k
