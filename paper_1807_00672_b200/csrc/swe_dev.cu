@@ -1180,6 +1180,11 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
                  const int* gcell, const int* gedge, double timeout_s) {
   if (!x) return fail_invalid("null context");
   if (x->linked) return fail_invalid("swe_dev_link: context is already linked");
+  if (const char* env = std::getenv("SWE_LINK_FAIL"))  // test hook: an IPC-less platform
+    if (std::atoi(env) == 1 + rank || std::atoi(env) == -1) {
+      g_last_error = "swe_dev_link: peer memory unavailable (SWE_LINK_FAIL)";
+      return SWE_CUDA;
+    }
   if (nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks || !peer_cells ||
       (!arenas && !ipc_handles) || n_push < 0 ||
       (n_push && (!push_cell || !push_rank || !push_ghost)))

@@ -299,14 +299,20 @@ class TorchExchange:
     def __init__(self, part, group=None):
         import torch.distributed as dist
         self.dist, self.part, self.group = dist, part, group
+        # gloo moves host memory only: device buffers are staged through the host
+        self.host_staged = dist.get_backend(group) == "gloo" and part.send_buf.is_cuda
 
     def halo(self):
         import torch
         p, dist = self.part, self.dist
         p.pack()
-        ops = []
+        ops, back = [], []
         for i, q in enumerate(p.lm.peers):  # plans are symmetric: both directions per peer
             sb, rb = p.send_block(i), p.recv_block(i)
+            if self.host_staged:
+                sb, dev_rb = sb.cpu(), rb
+                rb = torch.empty(rb.shape, dtype=rb.dtype)
+                back.append((dev_rb, rb))
             if sb.numel():
                 ops.append(dist.P2POp(dist.isend, sb, q, self.group))
             if rb.numel():
@@ -314,13 +320,16 @@ class TorchExchange:
         if ops:
             for r in dist.batch_isend_irecv(ops):
                 r.wait()
+        for dev_rb, host_rb in back:
+            dev_rb.copy_(host_rb)
         if p.send_buf.is_cuda:
             torch.cuda.synchronize(p.send_buf.device)
         p.unpack()
 
     def _reduce(self, x, op):
         import torch
-        t = torch.tensor([x], dtype=torch.float64, device=self.part.send_buf.device)
+        t = torch.tensor([x], dtype=torch.float64,
+                         device="cpu" if self.host_staged else self.part.send_buf.device)
         self.dist.all_reduce(t, op=op, group=self.group)
         return float(t.item())
 
@@ -514,17 +523,33 @@ def exchange_link_info(part_id: int, lm: LocalMesh, handle: bytes, group=None):
     return handles, cells, recv
 
 
+class LinkUnavailable(DeviceError):
+    """some rank could not map its peers' memory (CUDA IPC / peer access)"""
+
+
 def link_torch(part: LinkedPart, group=None, timeout_s: float = 60.0):
     """Link one part per rank (torchrun): part id == rank; peers' arenas are
-    mapped through CUDA IPC (NVLink peer memory on one node)."""
+    mapped through CUDA IPC (NVLink peer memory on one node).  Collective and
+    fail-safe: if any rank cannot link, every rank raises LinkUnavailable
+    (instead of some ranks waiting forever at a barrier)."""
+    import torch
     import torch.distributed as tdist
     rank, nr = tdist.get_rank(group), tdist.get_world_size(group)
     if part.lm.part != rank:
         raise ValueError("link_torch: the part id must equal the rank")
     _, handle = part.export()
     handles, cells, recv = exchange_link_info(rank, part.lm, handle, group)
-    part.link(rank, nr, cells, push_plan(part.lm, recv), handles=handles, timeout_s=timeout_s)
-    tdist.barrier(group)
+    err = ""
+    try:
+        part.link(rank, nr, cells, push_plan(part.lm, recv), handles=handles, timeout_s=timeout_s)
+    except DeviceError as e:
+        err = str(e)
+    backend = tdist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else "cpu"
+    ok = torch.tensor([0.0 if err else 1.0], device=dev)
+    tdist.all_reduce(ok, op=tdist.ReduceOp.MIN, group=group)
+    if ok.item() < 1.0:
+        raise LinkUnavailable(err or "a peer rank could not link (CUDA IPC / peer access)")
 
 
 def run_lockstep(parts, nsteps: int, t_end: float = 1e30):
@@ -594,4 +619,4 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
 
 __all__ = ["partition", "cost_weights", "measured_cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
-           "run_lockstep", "DeviceError"]
+           "run_lockstep", "DeviceError", "LinkUnavailable"]
