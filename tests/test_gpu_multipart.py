@@ -195,3 +195,44 @@ def test_linked_two_phase_single_rank_graph():
     assert bit_equal(recs[:, 2], ref["dts"])
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(got, k), ref[k]), k
+
+
+def _fail_worker(rank, world, port, q):
+    import os
+    import torch
+    import torch.distributed as tdist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), SWE_LINK_FAIL="2")
+    torch.cuda.set_device(0)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        sc, m, lms = _scenario_parts(world)
+        lp = dist.LinkedPart(lms[rank])
+        try:
+            dist.link_torch(lp, timeout_s=5.0)
+            q.put((rank, "linked"))
+        except dist.LinkUnavailable as e:
+            q.put((rank, "unavailable"))
+        tdist.barrier()
+        lp.close()
+    finally:
+        tdist.destroy_process_group()
+
+
+def test_link_failure_on_one_rank_is_seen_by_all():
+    """rank 1 cannot map peer memory: every rank raises LinkUnavailable
+    (bench.py then takes the host-driven path) instead of hanging"""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fail_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=300) for _ in range(2))
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert res == {0: "unavailable", 1: "unavailable"}
