@@ -81,7 +81,7 @@ struct swe_dev_ctx {
   long long rec_cap = 0;
   double *stage_h = nullptr, *stage_qx = nullptr, *stage_qy = nullptr;
   int grid_face = 0, grid_cell = 0, grid_tile = 0;
-  int tile_threads = 128;  // measured best with 256-cell tiles (r02)
+  int tile_threads = 128;  // measured best with 256-cell tiles
   int* halo_send = nullptr;  // device ids of the halo plan
   int* halo_recv = nullptr;
   size_t tile_smem = 0;
@@ -572,7 +572,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.C_own = (m->n_owned > 0 && m->n_owned <= C) ? m->n_owned : C;
   d.P = Phys{params->g, params->h_dry, params->cfl, params->dt_max, params->h_ref};
   if (const char* env = std::getenv("SWE_TILE_THREADS")) x->tile_threads = std::atoi(env) == 128 ? 128 : 256;
-  // tile size: at most 256 cells (measured best, r02), shrunk so the tiles
+  // tile size: at most 256 cells (measured best), shrunk so the tiles
   // fill whole waves of the persistent grid (a 1.28M-cell part has 4.2 waves
   // of 256-cell tiles: the last one 23% busy)
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;

@@ -23,7 +23,7 @@
 
 #include "swe_ctl.cuh"
 
-// resident-block budgets (registers) measured on B200 at 10M cells (r02):
+// resident-block budgets (registers) measured on B200 at 10M cells:
 // face 5 (48 regs), cell 4 (64), tile 4 x 256-thread equivalents (64 regs)
 #ifndef SWE_FACE_MINB
 #define SWE_FACE_MINB 5
@@ -248,12 +248,14 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 
 // ---------------------------------------------------------------------------
 // fused tile kernel.  Per tile of T Morton-consecutive cells: stage the
-// tile's state and bed in shared memory, evaluate the owned + halo edges into per-incidence contributions in shared
-// memory, update the cells.  Shared memory: state+bed [4T], contributions
-// [9T] -- kept small on purpose: the FP64 dependency chains of the flux need
+// tile's state and bed in shared memory, evaluate the owned + halo edges
+// into per-incidence contributions in shared memory, update the cells.
+// Tiles whose cells and ring are dry and at rest skip the edge evaluation
+// (exact).  Shared memory: state+bed [4T], contributions [9T]
+// -- kept small on purpose: the FP64 dependency chains of the flux need
 // resident warps more than staged data (a variant staging every array needed
 // 65 KB per 256-cell tile and ran 1.3x slower; a TMA bulk L2 prefetch of the
-// next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%, r02).
+// next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%).
 // ---------------------------------------------------------------------------
 __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
   return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
@@ -262,7 +264,7 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
 // LINK: linked context -- after the update, push the tile's cells that peers
 // hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
 // (Finalizing in the kernel's last block instead of a separate launch was
-// measured slower, r02: its register copies spill into the main loop.)
+// measured slower: its register copies spill into the main loop.)
 template <int NT, bool LINK>
 __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
   extern __shared__ double smem[];
