@@ -237,7 +237,8 @@ def run_b200_dist(args, rank, local, world):
     scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
     sc, mesh, setup_s = build_workload(args.config, scale, device=local)
     # equal work per GPU: cells weighted by the device's own dry-tile skip pattern
-    part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local))
+    part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local,
+                                                                  parts=world))
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
     try:
@@ -315,8 +316,10 @@ def run_b200_dist(args, rank, local, world):
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "config": workload_config(args.config, sc, mesh, 1, {
                    "parallelism": f"{world}-way cost-weighted RCB domain decomposition (cells "
-                                  f"of computed tiles {dist.COMPUTED_COST}x cells of skipped dry "
-                                  "tiles, measured on the device), one part per GPU; "
+                                  "of computed tiles weighted "
+                                  f"{dist.COMPUTED_COST_LARGE if mesh.n_cells / world >= dist.LARGE_PART_CELLS else dist.COMPUTED_COST}"
+                                  "x cells of skipped dry tiles, measured on the device), one "
+                                  "part per GPU; "
                                   "ghost states pushed peer-to-peer by the step kernel, CFL "
                                   "bound / outcome through device mailboxes (no host round "
                                   "trip per step)",

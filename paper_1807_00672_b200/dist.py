@@ -82,14 +82,24 @@ def cost_weights(state: FieldState, h_dry: float = 1e-6, wet_cost: float = WET_C
     return w
 
 
-COMPUTED_COST = 3.8  # computed / skipped tile cost per cell (calibrated on 2/4/8-part splits)
+# computed / skipped tile cost per cell, calibrated on B200 splits of the 10M
+# channel (tools/scaling_proxy.py): small parts (strong scaling, ~1-5M cells
+# per GPU) 3.8; large parts (weak scaling, ~10M per GPU) 7.5 -- a skipped run
+# of tiles amortises its per-tile latency better in a long kernel
+COMPUTED_COST = 3.8
+COMPUTED_COST_LARGE = 7.5
+LARGE_PART_CELLS = 8_000_000
 
 
 def measured_cost_weights(mesh: Mesh, state: FieldState, device: int = 0, steps: int = 2,
-                          computed_cost: float = COMPUTED_COST) -> np.ndarray:
+                          computed_cost: float | None = None, parts: int = 0) -> np.ndarray:
     """per-cell cost from the device's own skip pattern: run the whole mesh
     `steps` steps and weight cells in skipped dry tiles 1, all others
-    computed_cost (captures the wet front at tile granularity)"""
+    computed_cost (captures the wet front at tile granularity); by default
+    computed_cost follows the part size (mesh cells / parts)"""
+    if computed_cost is None:
+        large = parts > 0 and mesh.n_cells / parts >= LARGE_PART_CELLS
+        computed_cost = COMPUTED_COST_LARGE if large else COMPUTED_COST
     from .api import DeviceSolver
     s = DeviceSolver(mesh, device=device)
     try:

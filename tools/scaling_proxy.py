@@ -24,10 +24,44 @@ def time_part(lp, steps, torch):
     return e0.elapsed_time(e1) / steps
 
 
+def weak(torch, api, dist, steps):
+    """weak scaling: the channel scaled to N x 10M cells, N cost-weighted parts
+    timed one by one; projected efficiency = 10M single step / slowest part"""
+    out = {"mode": "weak"}
+    sc = api.make_scenario("channel", scale=1.0)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    one = dist.LinkedPart(dist.local_mesh(mesh, dist.partition(mesh, 1), 0))
+    one.set_state(sc.state)
+    t1 = time_part(one, steps, torch)
+    one.close()
+    del mesh, sc
+    out["ms_1"] = t1
+    for n in [int(x) for x in sys.argv[sys.argv.index("--weak") + 1].split(",")]:
+        sc = api.make_scenario("channel", scale=n ** 0.5)
+        mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+        cc = float(sys.argv[sys.argv.index("--cc") + 1]) if "--cc" in sys.argv else None
+        w = dist.measured_cost_weights(mesh, sc.state, parts=n, **({"computed_cost": cc} if cc else {}))
+        part = dist.partition(mesh, n, w)
+        ts, cells = [], []
+        for p in range(n):
+            lm = dist.local_mesh(mesh, part, p)
+            lp = dist.LinkedPart(lm)
+            lp.set_state(sc.state)
+            ts.append(time_part(lp, steps, torch))
+            cells.append(lm.n_owned)
+            lp.close()
+        out[f"N{n}"] = {"cells": mesh.n_cells, "ms_parts": ts, "owned_cells": cells,
+                        "ms_max": max(ts), "projected_efficiency_no_exchange": t1 / max(ts)}
+        del mesh, sc
+    print(json.dumps(out))
+
+
 def main():
     import torch
     from paper_1807_00672_b200 import api, dist
     steps = 100
+    if "--weak" in sys.argv:
+        return weak(torch, api, dist, steps)
     sc = api.make_scenario("channel", scale=1.0)
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
     out = {"cells": mesh.n_cells}
@@ -46,10 +80,12 @@ def main():
         out["partition"] = "cost-weighted RCB (wet/dry model)"
     if "--measured" in sys.argv:
         cc = float(sys.argv[sys.argv.index("--measured") + 1]) \
-            if len(sys.argv) > sys.argv.index("--measured") + 1 else dist.COMPUTED_COST
-        weights = dist.measured_cost_weights(mesh, sc.state, computed_cost=cc)
+            if len(sys.argv) > sys.argv.index("--measured") + 1 else None
         out["partition"] = f"cost-weighted RCB (measured skip pattern, computed tiles {cc}x)"
     for n in (2, 4, 8):
+        if "--measured" in sys.argv:
+            weights = dist.measured_cost_weights(mesh, sc.state, parts=n,
+                                                 **({"computed_cost": cc} if cc else {}))
         part = dist.partition(mesh, n, weights)
         ts, cells, wet = [], [], []
         for p in range(n):
