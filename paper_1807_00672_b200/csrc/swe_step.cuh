@@ -266,7 +266,10 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
 // (Finalizing in the kernel's last block instead of a separate launch was
 // measured slower: its register copies spill into the main loop.)
 template <int NT, bool LINK>
-__global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile(Dev d) {
+#ifndef SWE_TILE_BLOCKS
+#define SWE_TILE_BLOCKS(NT) (SWE_TILE_MINB * 256 / (NT))
+#endif
+__global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   extern __shared__ double smem[];
   Ctl* ctl = d.ctl;
   if (!ctl->active) return;
