@@ -714,12 +714,16 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     return bail(SWE_INVALID);
   }
   const void* ktile = tile_kernel(x->tile_threads, false, d.stage);
-  for (int L = 0; L < 2; ++L)
+  for (int L = 0; L < 2; ++L) {
     if (!cuda_ok(cudaFuncSetAttribute(tile_kernel(x->tile_threads, L, d.stage),
                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)x->tile_smem),
                  "tile smem attribute"))
       return bail(SWE_CUDA);
+    if (const char* env = std::getenv("SWE_CARVEOUT"))  // experiment: shared-memory share of L1
+      cudaFuncSetAttribute(tile_kernel(x->tile_threads, L, d.stage),
+                           cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env));
+  }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tile, ktile, x->tile_threads, x->tile_smem);
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
