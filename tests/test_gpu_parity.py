@@ -511,3 +511,30 @@ def test_dry_skip_long_runs_equal_no_skip(monkeypatch, config, scale, steps):
     assert bit_equal(ra, rb)
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(sa, k), getattr(sb, k)), k
+
+
+@pytest.mark.parametrize("config", ["channel", "sloping_wet_dry"])
+def test_full_size_steps_bitwise_vs_reference(refo, config):
+    """BASELINE configs [2] / [3] at FULL size (10.26M cells): 12 device steps
+    (dry-tile skipping on, Morton tiles) equal the reference's own
+    advance_step (oracle/_ref, all host threads) bit for bit -- state, dt,
+    max speed and the clip ledger's event count."""
+    import os
+    sc = api.make_scenario(config)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    s = api.DeviceSolver(mesh)
+    s.set_state(sc.state)
+    recs = s.advance(1e30, max_steps=12)
+    got, _, _ = s.get_state()
+    _, ev = s.ledger()
+    info = s.info()
+    s.close()
+    rm = refo.build_mesh(sc.raw.nodes, sc.raw.triangles, sc.bed, sc.manning)
+    r = rm.advance(sc.state.h, sc.state.qx, sc.state.qy, t_end=1e30, nsteps=12,
+                   threads=len(os.sched_getaffinity(0)))
+    assert r["rc"] == 0 and r["done"] == 12
+    assert info["dry_skip"] == 1 and info["skipped_tiles"] > 0
+    assert bit_equal(recs[:, 2], r["dts"]) and bit_equal(recs[:, 3], r["max_speeds"])
+    assert ev == r["clip_events"]
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), r[k]), k
