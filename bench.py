@@ -556,10 +556,13 @@ def run_b200(args):
            "config": workload_config(args.config, sc, mesh, world,
                                      {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
                                       "device_bytes": solver.memory_bytes()}),
-           "gpu_launches": (2 if info["fused"] else 3) * K + 2,
-           "gpu_launches_note": "k_set_params + one CUDA-graph launch = k_gate + K x ("
+           "gpu_launches": (2 if info["fused"] else 3) * info["graph_unroll"]
+                           * -(-K // info["graph_unroll"]) + 2,
+           "gpu_launches_note": "k_set_params + one CUDA-graph launch = k_gate + a conditional "
+                                f"WHILE node of ceil(K/{info['graph_unroll']}) iterations x "
+                                f"{info['graph_unroll']} x ("
                                 + ("k_tile" if info["fused"] else "k_face_c, k_cell_c")
-                                + ", k_finalize) in a conditional WHILE node "
+                                + ", k_finalize); steps past the stop exit at once "
                                 f"(host-side launch calls: {launches})",
            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,

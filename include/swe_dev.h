@@ -229,7 +229,8 @@ SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launch
 /* Layout facts: [0] fused?, [1] cells per tile, [2] tiles, [3] max slots per
  * tile, [4] halo edges, [5] tile grid, [6] face grid, [7] cell grid,
  * [8] tile shared-memory bytes, [9] edges, [10] dry-tile skipping on?,
- * [11] dry tiles skipped so far (n > 11 synchronises the context). */
+ * [11] dry tiles skipped so far (n > 11 synchronises the context),
+ * [12] steps per WHILE iteration of the run graph. */
 SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
 
 /* Per cell (reference numbering): 1 if dry-tile skipping will skip the cell's

@@ -93,6 +93,7 @@ struct swe_dev_ctx {
   bool linked = false;
   bool cfl_posted = false;  // link_phase: a CFL exchange awaits its wait
   bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
+  int graph_unroll = 4;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
   // asynchronous snapshots: device staging slots, copy stream, events
@@ -288,8 +289,13 @@ int build_graph(swe_dev_ctx* x) {
   CK(cudaStreamBeginCaptureToGraph(x->stream, body, nullptr, nullptr, 0,
                                    cudaStreamCaptureModeThreadLocal));
   const long long before = g_launches;
-  launch_update(x);
-  launch_finalize(x, x->cond, 1);
+  // the WHILE body holds `graph_unroll` steps: a step that finds the loop
+  // stopped exits at once, and the conditional node's per-iteration cost
+  // (~2-3 us) is shared (measured: -0.8% at 10M cells, -7% at 1M, -19% at 10k)
+  for (int u = 0; u < x->graph_unroll; ++u) {
+    launch_update(x);
+    launch_finalize(x, x->cond, 1);
+  }
   g_launches = before;  // captured, not launched
   cudaGraph_t captured = nullptr;
   CK(cudaStreamEndCapture(x->stream, &captured));
@@ -577,6 +583,7 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   // of 256-cell tiles: the last one 23% busy)
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
+  if (const char* env = std::getenv("SWE_GRAPH_UNROLL")) x->graph_unroll = std::max(1, std::atoi(env));
   d.skip = 1;  // dry-tile skipping (fused kernel); SWE_NO_DRY_SKIP=1 turns it off
   if (const char* env = std::getenv("SWE_NO_DRY_SKIP")) d.skip = std::atoi(env) == 0;
   // tile size: 224 cells, a sharp measured optimum on B200 (3-7%
@@ -1162,10 +1169,11 @@ int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
   if (!x || !out) return fail_invalid("null argument");
   if (n > 11)
     if (int rc = sync_ctl(x)) return rc;
-  const long long v[12] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
+  const long long v[13] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
                            x->grid_tile, x->grid_face, x->grid_cell, (long long)x->tile_smem,
-                           x->d.E, x->d.skip, n > 11 ? (long long)x->h_ctl->skipped : 0};
-  for (int i = 0; i < n && i < 12; ++i) out[i] = v[i];
+                           x->d.E, x->d.skip, n > 11 ? (long long)x->h_ctl->skipped : 0,
+                           x->graph_unroll};
+  for (int i = 0; i < n && i < 13; ++i) out[i] = v[i];
   return SWE_OK;
 }
 
