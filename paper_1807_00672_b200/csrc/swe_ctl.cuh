@@ -461,9 +461,10 @@ __device__ void post_outcome(const Dev& d, const Part& p, int kind) {
     d.ctl->bad_speed = kNone;
     d.ctl->xseq = tag;
   }
+  // the step kernel's halo pushes were fenced at system scope by their
+  // writers; this lane's slot write is ordered before its flag by the release
   for (int q = lane; q < L.nranks; q += 32) {
     L.box[q]->slot[tag & 1][L.rank] = x;
-    __threadfence_system();
     st_release_sys(&L.box[q]->flag[L.rank], tag);
   }
   __syncwarp();
@@ -570,6 +571,9 @@ __device__ __forceinline__ bool skip_mask_blocks(const Dev& d) {
       const int fl = nb < d.ntiles ? d.dryflag[nb] : 0;
       ok &= fl == f ? 1 : 0;
     }
+    // a tile whose cells peers hold as ghosts is computed, never skipped: its
+    // halo pushes run on the computed path (computing it is exact anyway)
+    if (d.L.nranks > 0 && d.L.tile_push[u + 1] > d.L.tile_push[u]) ok = 0;
     d.skipmask[u] = ok ? f : 0;
   }
   return true;

@@ -312,9 +312,10 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     const int c0 = t * T;
     const int nc = min(T, d.C_own - c0);
     const bool pre_skip = ahead && s_dec[it & 7] != 0;
-    if (!LINK && pre_skip) {
+    if (pre_skip) {
       // skipped tiles, fast path: a run of up to kAhead consecutive skipped
-      // tiles of this CTA in one round trip, no shared memory
+      // tiles of this CTA in one round trip, no shared memory (a tile with
+      // halo pushes is never in the skip mask)
       int run = 1;
       while (run < kAhead && s_dec[(it + run) & 7]) ++run;
       if (threadIdx.x == 0) {
