@@ -56,7 +56,7 @@ CONFIG_NOTE = {
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
     ap.add_argument("--config", default="channel", choices=list(CONFIG_NOTE))
@@ -94,7 +94,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "50"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -131,7 +131,7 @@ class ClockSampler:
             else:  # region shorter than the sampling period: nearest samples
                 mid = 0.5 * (self.window[0] + self.window[1])
                 rows = sorted(rows, key=lambda r: abs(r[0] - mid))[:3]
-                where = "nearest samples to a timed region shorter than the 50 ms sampling period"
+                where = "nearest samples to a timed region shorter than the 20 ms sampling period"
         rows = [r for _, r in rows]
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
