@@ -42,6 +42,11 @@ __device__ __forceinline__ double sel_max(double a, double b) { return (a < b) ?
 #ifndef SWE_ZERO_SAFE
 #define SWE_ZERO_SAFE 1
 #endif
+// velocity quotients as warp-uniform branches (dry or still cells skip the
+// division) rather than selects: measured -0.1..-2.8% and fewer spills
+#ifndef SWE_VEL_BRANCH
+#define SWE_VEL_BRANCH 1
+#endif
 __device__ __forceinline__ double div_rn(double a, double b) {
   double q;
   asm("div.rn.f64 %0, %1, %2;" : "=d"(q) : "d"(a), "d"(b));
@@ -59,7 +64,10 @@ __device__ __forceinline__ double qdiv(double a, double b) {
 // a / b for b known positive and finite (depths >= h_dry > 0, friction
 // denominators >= 1): only the numerator needs the guard (0 / b = a)
 __device__ __forceinline__ double qdivp(double a, double b) {
-#if SWE_ZERO_SAFE
+#if SWE_VEL_BRANCH
+  if (a == 0.0) return a;  // warps at rest skip the division
+  return div_rn(a, b);
+#elif SWE_ZERO_SAFE
   const bool z = a == 0.0;
   const double q = div_rn(z ? 1.0 : a, b);
   return z ? a : q;
@@ -83,10 +91,20 @@ __device__ __forceinline__ double qsqrt(double x) {
 // takes the division's special-operand slow path; the selected value is the
 // reference's exactly.
 __device__ __forceinline__ void vel(const Cons& u, double h_dry, double& vx, double& vy) {
+#if SWE_VEL_BRANCH
+  // a branch, not a select: warps of dry cells skip the divisions
+  vx = 0.0;
+  vy = 0.0;
+  if (!(u.h < h_dry)) {
+    vx = qdivp(u.qx, u.h);
+    vy = qdivp(u.qy, u.h);
+  }
+#else
   const bool dry = u.h < h_dry;
   const double hs = dry ? 1.0 : u.h;
   vx = dry ? 0.0 : qdivp(u.qx, hs);
   vy = dry ? 0.0 : qdivp(u.qy, hs);
+#endif
 }
 
 // physical_flux_normal(), kernels.hpp:21-27.
