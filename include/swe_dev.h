@@ -96,7 +96,10 @@ typedef struct {
                                       instead of the fused tile kernel */
 
 /* Uploads the mesh, renumbers it on the device, allocates the double-buffered
- * state and edge records.  device = CUDA ordinal. */
+ * state and edge records.  device = CUDA ordinal.  One context drives one GPU
+ * (SURVEY.md §8(b) sketched one context over n_gpus driven from one thread);
+ * a multi-GPU run is one context per GPU and process, joined by
+ * swe_dev_link (below), so every rank keeps its own stream and graph. */
 SWE_API int swe_dev_create(const swe_mesh_view* mesh, const swe_params* params, int device,
                    unsigned flags, swe_dev_ctx** out);
 SWE_API int swe_dev_destroy(swe_dev_ctx* ctx);
