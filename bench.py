@@ -530,12 +530,13 @@ def run_b200(args):
     peak, peak_src = load_peaks()
     if info["fused"]:
         # k_tile compulsory traffic: cell state/bed/area/n/r in (56 B) + state
-        # out (24 B); edge el, er, nx, ny, len, kl, kr (34 B); halo index (4 B)
+        # out (24 B); edge record {el|kl, er|kr} (8 B) + {nx, ny} (16 B) + len
+        # (8 B) = 32 B; halo index (4 B)
         # a dry tile skipped moves 40 B per cell: h and area in,
         # state out -- no edge data, no qx / qy / bed
         tile_ms = avg("tile")
         kernels = {"tile": tile_ms, "finalize": fin_ms}
-        full = 80 * C + 34 * E + 4 * info["halo_edges"]
+        full = 80 * C + 32 * E + 4 * info["halo_edges"]
         dom = ("tile", tile_ms, (1.0 - prof_skip) * full + prof_skip * 40 * C)
     else:
         # k_face_c: edge data 34 B + contributions out 48 B per edge, state+bed

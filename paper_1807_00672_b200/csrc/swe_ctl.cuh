@@ -122,6 +122,10 @@ struct Dev {
   const double *nx, *ny, *len;
   const int* e_orig;
   const unsigned char *kl, *kr;  // local index k of the edge in its left / right cell
+  // k_tile's edge records: ek = {el | kl << 30, er | kr << 30 (-1: wall)},
+  // enxy = {nx, ny}; one 8 B and one 16 B load instead of six (fused path)
+  const int2* ek;
+  const double2* enxy;
   // tiles of T consecutive cells (fused path)
   int T, ntiles, max_slots;  // max_slots: most edges (owned + halo) of one tile
   const int* eoff;  // [ntiles+1] owned edge range of each tile

@@ -491,6 +491,10 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
        cuda_ok(cudaMemsetAsync(kr, 0xff, E, s), "memset");
   k_local_index<<<blocks_for(C), kBlock, 0, s>>>(C, i0, i1, i2, kl, kr);
   k_local_check<<<blocks_for(E), kBlock, 0, s>>>(E, er, kl, kr, flags);
+  if (d.ek)
+    k_pack_edges<<<blocks_for(E), kBlock, 0, s>>>(E, el, er, kl, kr, d.nx, d.ny,
+                                                  const_cast<int2*>(d.ek),
+                                                  const_cast<double2*>(d.enxy));
   std::vector<int> h_eoff(d.ntiles + 1), h_hoff(d.ntiles + 1);
   ok = ok && cuda_ok(cudaGetLastError(), "local index") &&
        cuda_ok(cudaMemcpyAsync(h_eoff.data(), eoff, sizeof(int) * (d.ntiles + 1),
@@ -543,6 +547,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
       !m->edge_left || !m->edge_right || !m->nx || !m->ny || !m->len)
     return fail_invalid("swe_dev_create: missing mesh array");
   const int C = m->n_cells, E = m->n_edges;
+  if (C >= (1 << 30))  // packed edge records keep k in the top two bits
+    return fail_invalid("swe_dev_create: more than 2^30 - 1 cells");
   for (int e = 0; e < E; ++e) {
     const int l = m->edge_left[e], r = m->edge_right[e];
     if (l < 0 || l >= C || r < -1 || r >= C)
@@ -632,6 +638,14 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.halo = x->alloc<int>(E);
   d.kl = x->alloc<unsigned char>(E);
   d.kr = x->alloc<unsigned char>(E);
+  if (x->fused) {
+    d.ek = x->alloc<int2>(E);
+    d.enxy = x->alloc<double2>(E);
+    if (!d.enxy) {
+      g_last_error = "swe_dev_create: cudaMalloc failed";
+      return bail(SWE_CUDA);
+    }
+  }
   // state arrays + mailbox in one allocation (the arena peers map)
   x->arena_bytes = arena_offset(C, 6);
   x->arena = x->alloc<char>(x->arena_bytes);

@@ -216,6 +216,17 @@ __global__ void k_local_check(int E, const int* er, const unsigned char* kl,
   if (kl[e] > 2 || (er[e] >= 0 && kr[e] > 2)) atomicExch(bad, 2);
 }
 
+// k_tile's packed edge records (Dev::ek, Dev::enxy); cells < 2^30 (checked)
+__global__ void k_pack_edges(int E, const int* el, const int* er, const unsigned char* kl,
+                             const unsigned char* kr, const double* nx, const double* ny,
+                             int2* ek, double2* enxy) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  const int r = er[e];
+  ek[e] = make_int2(el[e] | ((int)kl[e] << 30), r < 0 ? -1 : (r | ((int)kr[e] << 30)));
+  enxy[e] = make_double2(nx[e], ny[e]);
+}
+
 // multi-device halo exchange: owned cells' current state -> buffer (h, qx, qy
 // interleaved), buffer -> ghost cells' current state
 __global__ void k_halo_pack(Dev d, double* buf) {

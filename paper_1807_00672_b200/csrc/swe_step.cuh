@@ -378,9 +378,11 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     // owned + halo edges -> contributions of the in-tile sides
     for (int j = threadIdx.x; j < (skip ? 0 : ns); j += NT) {
       const int e = j < no ? e0 + j : __ldg(d.halo + h0 + (j - no));
-      const int cl = __ldg(d.el + e), cr = __ldg(d.er + e);
-      const double nx = __ldg(d.nx + e), ny = __ldg(d.ny + e), len = __ldg(d.len + e);
-      const bool w = cr < 0;
+      const int2 ek = __ldg(d.ek + e);
+      const double2 nn = __ldg(d.enxy + e);
+      const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
+      const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
+      const bool w = ek.y == -1;
       const int il = cl - c0, ir = (w ? cl : cr) - c0;
       const bool inL = (unsigned)il < (unsigned)nc, inR = !w && (unsigned)ir < (unsigned)nc;
       Cons uL, uR;
@@ -406,13 +408,13 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         continue;
       }
       if (inL) {
-        const int s = 3 * il + __ldg(d.kl + e);
+        const int s = 3 * il + (int)((unsigned)ek.x >> 30);
         tm[s] = et.lm;
         tx[s] = et.lx;
         ty[s] = et.ly;
       }
       if (inR) {
-        const int s = 3 * ir + __ldg(d.kr + e);
+        const int s = 3 * ir + (int)((unsigned)ek.y >> 30);
         tm[s] = et.rm;
         tx[s] = et.rx;
         ty[s] = et.ry;
