@@ -106,6 +106,10 @@ struct Link {
   unsigned long long timeout_ns;
 };
 
+struct __align__(32) CellGeo {
+  double z, area, man, inr;
+};
+
 struct Dev {
   int C, E;
   int C_own;  // cells [0, C_own) are owned (updated); [C_own, C) are ghosts of a multi-device run
@@ -126,6 +130,8 @@ struct Dev {
   // enxy = {nx, ny}; one 8 B and one 16 B load instead of six (fused path)
   const int2* ek;
   const double2* enxy;
+  // k_tile's cell record {z, area, manning, inradius}: one 32 B load (fused path)
+  const struct CellGeo* cg;
   // tiles of T consecutive cells (fused path)
   int T, ntiles, max_slots;  // max_slots: most edges (owned + halo) of one tile
   const int* eoff;  // [ntiles+1] owned edge range of each tile

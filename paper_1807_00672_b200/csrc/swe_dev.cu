@@ -641,7 +641,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   if (x->fused) {
     d.ek = x->alloc<int2>(E);
     d.enxy = x->alloc<double2>(E);
-    if (!d.enxy) {
+    d.cg = x->alloc<CellGeo>(C);
+    if (!d.enxy || !d.cg) {
       g_last_error = "swe_dev_create: cudaMalloc failed";
       return bail(SWE_CUDA);
     }
@@ -689,6 +690,11 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   d.rec = x->rec;
 
   if (int rc = preprocess(x, m)) return bail(rc);
+  if (d.cg) {
+    k_pack_cells<<<blocks_for(C), kBlock, 0, x->stream>>>(C, d.z, d.area, d.man, d.inr,
+                                                        const_cast<CellGeo*>(d.cg));
+    if (!cuda_ok(cudaGetLastError(), "k_pack_cells")) return bail(SWE_CUDA);
+  }
   if (!x->fused || d.stage) d.skip = 0;
   if (d.skip)
     if (int rc = build_tile_neighbours(x)) return bail(rc);

@@ -227,6 +227,14 @@ __global__ void k_pack_edges(int E, const int* el, const int* er, const unsigned
   enxy[e] = make_double2(nx[e], ny[e]);
 }
 
+// k_tile's cell records (Dev::cg)
+__global__ void k_pack_cells(int C, const double* z, const double* area, const double* man,
+                             const double* inr, CellGeo* cg) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  cg[c] = CellGeo{z[c], area[c], man[c], inr[c]};
+}
+
 // multi-device halo exchange: owned cells' current state -> buffer (h, qx, qy
 // interleaved), buffer -> ghost cells' current state
 __global__ void k_halo_pack(Dev d, double* buf) {

@@ -257,6 +257,17 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // 65 KB per 256-cell tile and ran 1.3x slower; a TMA bulk L2 prefetch of the
 // next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%).
 // ---------------------------------------------------------------------------
+#ifndef SWE_CELL_GEO
+#define SWE_CELL_GEO 1
+#endif
+// one 256-bit read-only load of a cell record (sm_100: LDG.E.ENL2.256)
+__device__ __forceinline__ CellGeo ldg_geo(const CellGeo* p) {
+  CellGeo g;
+  asm("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];"
+      : "=d"(g.z), "=d"(g.area), "=d"(g.man), "=d"(g.inr)
+      : "l"(p));
+  return g;
+}
 __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
   return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
 }
@@ -347,7 +358,11 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (!pre_skip) {
         sq[i] = QX[c0 + i];
         sr[i] = QY[c0 + i];
+#if SWE_CELL_GEO
+        sz[i] = ldg_geo(d.cg + c0 + i).z;  // area, n, r come along (read at the update)
+#else
         sz[i] = __ldg(d.z + c0 + i);
+#endif
       }
     }
     const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
@@ -444,7 +459,13 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         ax += tx[3 * i + k];
         ay += ty[3 * i + k];
       }
+#if SWE_CELL_GEO
+      const CellGeo g = ldg_geo(d.cg + c0 + i);
+      const Cons u = cell_finish_v(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, g.area, g.man,
+                                   g.inr, NH, NQX, NQY, a);
+#else
       const Cons u = cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
+#endif
       dry &= (0.0 <= u.h && u.h < P.h_dry) ? 1 : 0;
       if (LINK && p1 > p0) {  // the tile's new state, for the push below
         sh[i] = u.h;
