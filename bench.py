@@ -549,11 +549,12 @@ def run_b200(args):
     achieved = dom[2] / (dom[1] / 1e3) / 1e9
     step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical two-phase B_step
     step_eff = (1.0 - skip_frac) * step_bytes + skip_frac * 40 * C  # skipped tiles: 40 B/cell
-    traffic = None
+    traffic, limiter = None, None
     prof = ROOT / "profiles" / "traffic.json"
     if prof.exists():
         try:
-            traffic = json.loads(prof.read_text()).get(dom[0])
+            tj = json.loads(prof.read_text())
+            traffic, limiter = tj.get(dom[0]), tj.get(dom[0] + "_limiter")
         except Exception:
             traffic = None
 
@@ -574,6 +575,7 @@ def run_b200(args):
            "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
                         "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                         "peak_source": peak_src,
+                        "limiter": limiter,
                         "algorithmic_bytes_per_launch": dom[2],
                         "kernel_ms": kernels,
                         "layout": info,
