@@ -257,6 +257,40 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // 65 KB per 256-cell tile and ran 1.3x slower; a TMA bulk L2 prefetch of the
 // next tile's ranges (cp.async.bulk.prefetch.L2) cost 6%).
 // ---------------------------------------------------------------------------
+// streamed loads that no other warp of the CTA re-reads kept out of L1
+// (SWE_L1_HINTS=1: ld.global.L1::no_allocate for the edge records and the
+// staged state) -- measured no faster than the default allocation
+#ifndef SWE_L1_HINTS
+#define SWE_L1_HINTS 0
+#endif
+#if SWE_L1_HINTS
+__device__ __forceinline__ double ld_na(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld_na(const double2* p) {
+  double2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ int2 ld_na(const int2* p) {
+  int2 v;
+  asm("ld.global.nc.L1::no_allocate.v2.s32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+  return v;
+}
+// state of the current step: written by the previous launch, read-only here
+__device__ __forceinline__ double ld_na_state(const double* p) {
+  double v;
+  asm("ld.global.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+#define SWE_LD_STREAM(p) ld_na(p)
+#define SWE_LD_STATE(p) ld_na_state(p)
+#else
+#define SWE_LD_STREAM(p) __ldg(p)
+#define SWE_LD_STATE(p) (*(p))
+#endif
 #ifndef SWE_CELL_GEO
 #define SWE_CELL_GEO 1
 #endif
@@ -354,10 +388,10 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       continue;
     }
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile (a skipped one needs h only)
-      sh[i] = H[c0 + i];
+      sh[i] = SWE_LD_STATE(H + c0 + i);
       if (!pre_skip) {
-        sq[i] = QX[c0 + i];
-        sr[i] = QY[c0 + i];
+        sq[i] = SWE_LD_STATE(QX + c0 + i);
+        sr[i] = SWE_LD_STATE(QY + c0 + i);
 #if SWE_CELL_GEO
         sz[i] = ldg_geo(d.cg + c0 + i).z;  // area, n, r come along (read at the update)
 #else
@@ -393,9 +427,9 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     // owned + halo edges -> contributions of the in-tile sides
     for (int j = threadIdx.x; j < (skip ? 0 : ns); j += NT) {
       const int e = j < no ? e0 + j : __ldg(d.halo + h0 + (j - no));
-      const int2 ek = __ldg(d.ek + e);
-      const double2 nn = __ldg(d.enxy + e);
-      const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
+      const int2 ek = SWE_LD_STREAM(d.ek + e);
+      const double2 nn = SWE_LD_STREAM(d.enxy + e);
+      const double nx = nn.x, ny = nn.y, len = SWE_LD_STREAM(d.len + e);
       const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
       const bool w = ek.y == -1;
       const int il = cl - c0, ir = (w ? cl : cr) - c0;
