@@ -247,6 +247,7 @@ def run_b200_dist(args, rank, local, world):
                                                                   parts=world))
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
+    U = api.DeviceSolver.info(lp)["graph_unroll"]  # steps per WHILE iteration
     try:
         dist.link_torch(lp)
     except dist.LinkUnavailable as e:  # every rank takes this branch together
@@ -332,10 +333,11 @@ def run_b200_dist(args, rank, local, world):
                    "cells_per_gpu_max": int(np.bincount(part).max()),
                    "cells_per_gpu_min": int(np.bincount(part).min()),
                    "halo_cells_rank0": int(lm.n_cells - lm.n_owned), "setup_s": round(setup_s, 2)}),
-               "gpu_launches": 2 * K + 2,
+               "gpu_launches": 2 * U * -(-K // U) + 2,
                "gpu_launches_note": "per rank: k_set_params + one CUDA-graph launch = k_gate + "
-                                    "K x (k_tile with halo push, k_exchange) in a conditional "
-                                    "WHILE node",
+                                    f"a conditional WHILE node of ceil(K/{U}) iterations x {U} x "
+                                    "(k_tile with halo push, k_exchange); steps past the stop "
+                                    "exit at once",
                "clocks": clk.summary() if clk else None,
                "roofline": dist_roofline(mesh, K, ms, world, skip_frac),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,

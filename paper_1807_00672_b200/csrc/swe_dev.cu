@@ -93,7 +93,7 @@ struct swe_dev_ctx {
   bool linked = false;
   bool cfl_posted = false;  // link_phase: a CFL exchange awaits its wait
   bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
-  int graph_unroll = 4;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
+  int graph_unroll = 8;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
   // asynchronous snapshots: device staging slots, copy stream, events
@@ -291,7 +291,9 @@ int build_graph(swe_dev_ctx* x) {
   const long long before = g_launches;
   // the WHILE body holds `graph_unroll` steps: a step that finds the loop
   // stopped exits at once, and the conditional node's per-iteration cost
-  // (~2-3 us) is shared (measured: -0.8% at 10M cells, -7% at 1M, -19% at 10k)
+  // (~2-3 us) is shared (measured 1 -> 4 steps: -0.8% at 10M cells, -7% at 1M,
+  // -19% at 10k; 4 -> 8: -0.5%, -1.5%, -4%; an advance() that stops mid-body
+  // pays <= 7 no-op step pairs, ~2.5 us each)
   for (int u = 0; u < x->graph_unroll; ++u) {
     launch_update(x);
     launch_finalize(x, x->cond, 1);
