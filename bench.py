@@ -615,19 +615,21 @@ def no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch):
         s = api.DeviceSolver(mesh, device=local)
     finally:
         del os.environ["SWE_NO_DRY_SKIP"]
-    s.set_state(sc.state)
-    s.advance(t_end=horizon, max_steps=step0)
     st = torch.cuda.ExternalStream(s.stream, device=local)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(st)
-    s.advance_async(t_end=horizon, max_steps=step0 + K)
-    e1.record(st)
-    torch.cuda.synchronize()
-    s.records()
-    ms = e0.elapsed_time(e1) / K
+    best = float("inf")
+    for _ in range(2):  # the first pass also brings the clocks back up after setup
+        s.set_state(sc.state)
+        s.advance(t_end=horizon, max_steps=step0)
+        torch.cuda.synchronize()
+        e0.record(st)
+        s.advance_async(t_end=horizon, max_steps=step0 + K)
+        e1.record(st)
+        torch.cuda.synchronize()
+        s.records()
+        best = min(best, e0.elapsed_time(e1) / K)
     s.close()
-    return ms
+    return best
 
 
 def e2e_run(api, solver, sc, K, horizon, torch):
