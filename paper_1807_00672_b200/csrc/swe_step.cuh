@@ -260,6 +260,9 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // streamed loads that no other warp of the CTA re-reads kept out of L1
 // (SWE_L1_HINTS=1: ld.global.L1::no_allocate for the edge records and the
 // staged state) -- measured no faster than the default allocation
+#ifndef SWE_STORE_EARLY
+#define SWE_STORE_EARLY 1
+#endif
 #ifndef SWE_L1_HINTS
 #define SWE_L1_HINTS 0
 #endif
@@ -451,6 +454,39 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         uR = Cons{__ldg(H + c), __ldg(QX + c), __ldg(QY + c)};
         zr = __ldg(d.z + c);
       }
+#if SWE_STORE_EARLY
+      // edge_terms() inlined with every contribution stored as soon as it is
+      // formed (shorter live ranges than a six-value record)
+      if (uL.h < 0.0 || (!w && uR.h < 0.0)) {  // engine.hpp:147-153
+        atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
+        continue;
+      }
+      const double hg = 0.5 * P.g;
+      const int sl = 3 * il + (int)((unsigned)ek.x >> 30);
+      if (!w) {
+        double f0, lx, ly, rx, ry;
+        interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
+        if (inL) {
+          const double ownL = (hg * uL.h) * uL.h;
+          tm[sl] = f0 * len;
+          tx[sl] = (lx - ownL * nx) * len;
+          ty[sl] = (ly - ownL * ny) * len;
+        }
+        if (inR) {
+          const int sr = 3 * ir + (int)((unsigned)ek.y >> 30);
+          const double ownR = (hg * uR.h) * uR.h;
+          tm[sr] = (-f0) * len;  // right.mass = -f.mass
+          tx[sr] = (rx - ownR * (-nx)) * len;
+          ty[sr] = (ry - ownR * (-ny)) * len;
+        }
+      } else if (inL) {
+        const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
+        const double ownL = (hg * uL.h) * uL.h;
+        tm[sl] = f.m * len;
+        tx[sl] = (f.fx - ownL * nx) * len;
+        ty[sl] = (f.fy - ownL * ny) * len;
+      }
+#else
       EdgeTerms et;
       if (!edge_terms(uL, zl, uR, zr, w, nx, ny, len, P, et)) {
         atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
@@ -468,6 +504,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         tx[s] = et.rx;
         ty[s] = et.ry;
       }
+#endif
     }
     __syncthreads();
 
