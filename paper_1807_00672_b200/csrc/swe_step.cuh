@@ -260,6 +260,9 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // streamed loads that no other warp of the CTA re-reads kept out of L1
 // (SWE_L1_HINTS=1: ld.global.L1::no_allocate for the edge records and the
 // staged state) -- measured no faster than the default allocation
+#ifndef SWE_RELOAD
+#define SWE_RELOAD 1
+#endif
 #ifndef SWE_STORE_EARLY
 #define SWE_STORE_EARLY 1
 #endif
@@ -466,6 +469,28 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (!w) {
         double f0, lx, ly, rx, ry;
         interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
+#if SWE_RELOAD
+        // the edge's index record and length are re-read (L1) rather than
+        // held in registers across the Riemann solver
+        (void)inR;
+        const int2 ek2 = __ldg(d.ek + e);
+        const double len2 = __ldg(d.len + e);
+        const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
+        if ((unsigned)il2 < (unsigned)nc) {
+          const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
+          const double ownL = (hg * uL.h) * uL.h;
+          tm[s2] = f0 * len2;
+          tx[s2] = (lx - ownL * nx) * len2;
+          ty[s2] = (ly - ownL * ny) * len2;
+        }
+        if ((unsigned)ir2 < (unsigned)nc) {
+          const int sr = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
+          const double ownR = (hg * uR.h) * uR.h;
+          tm[sr] = (-f0) * len2;  // right.mass = -f.mass
+          tx[sr] = (rx - ownR * (-nx)) * len2;
+          ty[sr] = (ry - ownR * (-ny)) * len2;
+        }
+#else
         if (inL) {
           const double ownL = (hg * uL.h) * uL.h;
           tm[sl] = f0 * len;
@@ -479,6 +504,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
           tx[sr] = (rx - ownR * (-nx)) * len;
           ty[sr] = (ry - ownR * (-ny)) * len;
         }
+#endif
       } else if (inL) {
         const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
         const double ownL = (hg * uL.h) * uL.h;
