@@ -620,7 +620,8 @@ def no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch):
     best = float("inf")
     for _ in range(2):  # the first pass also brings the clocks back up after setup
         s.set_state(sc.state)
-        s.advance(t_end=horizon, max_steps=step0)
+        while s.clock()[1] < step0:  # in chunks: one advance() keeps at most 2^16 records
+            s.advance(t_end=horizon, max_steps=min(step0, s.clock()[1] + 50_000))
         torch.cuda.synchronize()
         e0.record(st)
         s.advance_async(t_end=horizon, max_steps=step0 + K)
