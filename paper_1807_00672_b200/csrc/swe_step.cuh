@@ -260,12 +260,6 @@ __global__ void __launch_bounds__(kBlock) k_push(Dev d) {
 // streamed loads that no other warp of the CTA re-reads kept out of L1
 // (SWE_L1_HINTS=1: ld.global.L1::no_allocate for the edge records and the
 // staged state) -- measured no faster than the default allocation
-#ifndef SWE_RELOAD
-#define SWE_RELOAD 1
-#endif
-#ifndef SWE_STORE_EARLY
-#define SWE_STORE_EARLY 1
-#endif
 #ifndef SWE_L1_HINTS
 #define SWE_L1_HINTS 0
 #endif
@@ -296,9 +290,6 @@ __device__ __forceinline__ double ld_na_state(const double* p) {
 #else
 #define SWE_LD_STREAM(p) __ldg(p)
 #define SWE_LD_STATE(p) (*(p))
-#endif
-#ifndef SWE_CELL_GEO
-#define SWE_CELL_GEO 1
 #endif
 // one 256-bit read-only load of a cell record (sm_100: LDG.E.ENL2.256)
 __device__ __forceinline__ CellGeo ldg_geo(const CellGeo* p) {
@@ -398,11 +389,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (!pre_skip) {
         sq[i] = SWE_LD_STATE(QX + c0 + i);
         sr[i] = SWE_LD_STATE(QY + c0 + i);
-#if SWE_CELL_GEO
         sz[i] = ldg_geo(d.cg + c0 + i).z;  // area, n, r come along (read at the update)
-#else
-        sz[i] = __ldg(d.z + c0 + i);
-#endif
       }
     }
     const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
@@ -457,7 +444,6 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         uR = Cons{__ldg(H + c), __ldg(QX + c), __ldg(QY + c)};
         zr = __ldg(d.z + c);
       }
-#if SWE_STORE_EARLY
       // edge_terms() inlined with every contribution stored as soon as it is
       // formed (shorter live ranges than a six-value record)
       if (uL.h < 0.0 || (!w && uR.h < 0.0)) {  // engine.hpp:147-153
@@ -469,7 +455,6 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (!w) {
         double f0, lx, ly, rx, ry;
         interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
-#if SWE_RELOAD
         // the edge's index record and length are re-read (L1) rather than
         // held in registers across the Riemann solver
         (void)inR;
@@ -490,21 +475,6 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
           tx[sr] = (rx - ownR * (-nx)) * len2;
           ty[sr] = (ry - ownR * (-ny)) * len2;
         }
-#else
-        if (inL) {
-          const double ownL = (hg * uL.h) * uL.h;
-          tm[sl] = f0 * len;
-          tx[sl] = (lx - ownL * nx) * len;
-          ty[sl] = (ly - ownL * ny) * len;
-        }
-        if (inR) {
-          const int sr = 3 * ir + (int)((unsigned)ek.y >> 30);
-          const double ownR = (hg * uR.h) * uR.h;
-          tm[sr] = (-f0) * len;  // right.mass = -f.mass
-          tx[sr] = (rx - ownR * (-nx)) * len;
-          ty[sr] = (ry - ownR * (-ny)) * len;
-        }
-#endif
       } else if (inL) {
         const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
         const double ownL = (hg * uL.h) * uL.h;
@@ -512,25 +482,6 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         tx[sl] = (f.fx - ownL * nx) * len;
         ty[sl] = (f.fy - ownL * ny) * len;
       }
-#else
-      EdgeTerms et;
-      if (!edge_terms(uL, zl, uR, zr, w, nx, ny, len, P, et)) {
-        atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
-        continue;
-      }
-      if (inL) {
-        const int s = 3 * il + (int)((unsigned)ek.x >> 30);
-        tm[s] = et.lm;
-        tx[s] = et.lx;
-        ty[s] = et.ly;
-      }
-      if (inR) {
-        const int s = 3 * ir + (int)((unsigned)ek.y >> 30);
-        tm[s] = et.rm;
-        tx[s] = et.rx;
-        ty[s] = et.ry;
-      }
-#endif
     }
     __syncthreads();
 
@@ -556,13 +507,9 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         ax += tx[3 * i + k];
         ay += ty[3 * i + k];
       }
-#if SWE_CELL_GEO
       const CellGeo g = ldg_geo(d.cg + c0 + i);
       const Cons u = cell_finish_v(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, g.area, g.man,
                                    g.inr, NH, NQX, NQY, a);
-#else
-      const Cons u = cell_finish(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, NH, NQX, NQY, a);
-#endif
       dry &= (0.0 <= u.h && u.h < P.h_dry) ? 1 : 0;
       if (LINK && p1 > p0) {  // the tile's new state, for the push below
         sh[i] = u.h;
