@@ -167,7 +167,10 @@ def workload_config(name, sc, mesh, world, note_extra=None):
     cfg = {"workload": f"{name} ({CONFIG_NOTE[name]})", "cells": mesh.n_cells,
            "edges": mesh.n_edges, "boundary_edges": mesh.n_boundary_edges,
            "mesh": "unstructured: jittered nodes, random diagonals, random node/cell numbering",
-           "l2": "inputs larger than L2 (state + mesh ~= 300 B/cell >> 126 MB)",
+           "l2": ("inputs larger than L2 (state + mesh ~= 300 B/cell >> 126 MB)"
+                  if 300 * mesh.n_cells > 2 * 126e6 else
+                  f"inputs fit in L2 (~{300 * mesh.n_cells / 1e6:.0f} MB of state + mesh): "
+                  "resident across steps as in any run of this size; not flushed"),
            "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"}
     if note_extra:
         cfg.update(note_extra)

@@ -1,0 +1,52 @@
+"""bench.py's JSON contract, checked on the CPU through the reference arm
+(`--impl reference`: the reference compiled in place, oracle/_ref) on the
+10k-cell BASELINE config [0]; the B200 arm's line carries the same keys plus
+roofline / clocks / gpu_launches (checked on the GPU box by the driver)."""
+import json
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+from oracle.pyoracle import RefOracle
+
+pytestmark = pytest.mark.skipif(not RefOracle.available(), reason="oracle/_ref not built")
+
+
+def run_bench(*args):
+    out = subprocess.run([sys.executable, str(ROOT / "bench.py"), *args], cwd=ROOT,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    return json.loads(lines[0])
+
+
+def test_reference_arm_line():
+    d = run_bench("--impl", "reference", "--config", "circular_dam_break", "--steps", "2",
+                  "--warmup", "1")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "cpu_baseline", "e2e"):
+        assert k in d, k
+    assert d["impl"] == "reference" and d["value"] > 0 and d["unit"] == "cell-updates/s"
+    assert d["higher_is_better"] is True and d["dtype"] == "f64" and d["vs_baseline"] is None
+    assert d["steps"] == 2 and d["n_gpus"] == 1
+    assert d["config"]["workload"].startswith("circular_dam_break") and "model" not in d["config"]
+    assert d["config"]["cells"] == 10082
+    cb = d["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["cores"] >= 1 and cb["value"] == d["value"]
+    e2e = d["e2e"]
+    assert e2e["value"] == d["value"] and e2e["h2d_bytes_per_step"] == 0
+    assert e2e["d2h_bytes_per_step"] == 0
+
+
+def test_reference_arm_bounds_its_sample():
+    """any --steps: at most bench.REF_MAX_STEPS timed steps, reported per step"""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    d = run_bench("--impl", "reference", "--config", "circular_dam_break", "--steps",
+                  str(bench.REF_MAX_STEPS + 5), "--warmup", "1")
+    assert d["steps"] == bench.REF_MAX_STEPS + 5
+    assert f"{bench.REF_MAX_STEPS} timed steps" in d["cpu_baseline"]["sample"]
