@@ -19,6 +19,31 @@ __device__ __forceinline__ unsigned spread16(unsigned v) {
   return v;
 }
 
+// SWE_HILBERT=1 orders the cells along a Hilbert curve instead (experiment:
+// fewer tile-crossing edges, 9.5% vs 10.1% of E at 224-cell tiles)
+#ifndef SWE_HILBERT
+#define SWE_HILBERT 0
+#endif
+
+// 32-bit Hilbert index of (x, y) on a 65536^2 grid
+__device__ __forceinline__ unsigned hilbert16(unsigned x, unsigned y) {
+  unsigned d = 0;
+  for (unsigned s = 1u << 15; s > 0; s >>= 1) {
+    const unsigned rx = (x & s) ? 1u : 0u, ry = (y & s) ? 1u : 0u;
+    d += s * s * ((3u * rx) ^ ry);
+    if (ry == 0) {
+      if (rx == 1) {
+        x = 65535u - x;
+        y = 65535u - y;
+      }
+      const unsigned t = x;
+      x = y;
+      y = t;
+    }
+  }
+  return d;
+}
+
 // 32-bit Morton code of the centroid on a 65536^2 grid over the bounding box
 __global__ void k_morton(int C, const double* cx, const double* cy, double x0, double y0, double s,
                          unsigned* key, int* idx) {
@@ -26,7 +51,11 @@ __global__ void k_morton(int C, const double* cx, const double* cy, double x0, d
   if (c >= C) return;
   const double fx = fmin(fmax((cx[c] - x0) * s, 0.0), 65535.0);
   const double fy = fmin(fmax((cy[c] - y0) * s, 0.0), 65535.0);
+#if SWE_HILBERT
+  key[c] = hilbert16((unsigned)fx, (unsigned)fy);
+#else
   key[c] = spread16((unsigned)fx) | (spread16((unsigned)fy) << 1);
+#endif
   idx[c] = c;
 }
 
