@@ -410,7 +410,8 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   int* c_new = const_cast<int*>(d.c_new);
   int* e_orig = const_cast<int*>(d.e_orig);
 
-  // 1. cells: Morton order of the owned cells' centroids (stable: ties keep
+  // 1. cells: space-filling-curve order (SWE_HILBERT) of the owned cells'
+  //    centroids (stable: ties keep
   //    reference order); ghost cells keep their place after the owned ones
   const int Co = d.C_own;
   const bool morton = !(x->flags & SWE_FLAG_IDENTITY_ORDER) && m->cx && m->cy;
@@ -430,8 +431,15 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
     unsigned* kout = (unsigned*)k64b;
     ok = dcx && dcy && up(dcx, m->cx, sizeof(double) * Co) && up(dcy, m->cy, sizeof(double) * Co);
     if (ok) {
+#if SWE_HILBERT == 2
+      const double side = std::max(std::min(x1 - x0, y1 - y0), span / 255.0) * (1.0 + 1e-9);
+      k_hilbert_blocks<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
+                                                          side > 0 ? side : 1.0,
+                                                          (y1 - y0) > (x1 - x0), kin, idx);
+#else
       k_morton<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
                                                   span > 0 ? 65535.0 / span : 0.0, kin, idx);
+#endif
       ok = radix_sort(tmp, kin, kout, idx, c_orig, Co, 32, s);
     }
   }
