@@ -15,7 +15,8 @@ reference's bench harness counts it (bench.hpp:173: cells * steps / wall).
 value     K steps with the state resident in HBM (one CUDA graph launch),
           device time (CUDA events on the solver's stream), max over ranks.
 e2e       the same K steps through the public C-ABI from pinned HOST buffers:
-          upload of the initial state, the K-step run with its per-step stats
+          upload of the state at value's first timed step (copied out before
+          the timed region), the K-step run with its per-step stats
           records copied back, download of the final state -- all inside the
           timed region (the reference run()'s contract, engine.hpp:335-394).
 roofline  the dominant kernel's algorithmic bytes per launch (SURVEY.md §8(d):
@@ -494,6 +495,8 @@ def run_b200(args):
         solver.advance(t_end=horizon, max_steps=s_now + 50)
     _, step0 = solver.clock()
     skipped0 = solver.info()["skipped_tiles"]
+    # e2e replays the same K steps from this state (untimed copy-out here)
+    e2e_start = None if args.no_e2e else solver.get_state()
 
     stream = torch.cuda.ExternalStream(solver.stream, device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -602,7 +605,7 @@ def run_b200(args):
             "step_frac_without_skip": step_bytes / (ms_ns / 1e3) / 1e9 / peak}
 
     if not args.no_e2e:
-        out["e2e"] = e2e_run(api, solver, sc, K, horizon, torch)
+        out["e2e"] = e2e_run(api, solver, e2e_start, K, horizon, torch)
     if rank == 0 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(sc, mesh, args)
     if rank == 0:
@@ -636,19 +639,21 @@ def no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch):
     return best
 
 
-def e2e_run(api, solver, sc, K, horizon, torch):
+def e2e_run(api, solver, start, K, horizon, torch):
     """Public C-ABI with pinned host buffers: H2D state, K steps with per-step
-    stats records back to the host, D2H final state."""
+    stats records back to the host, D2H final state.  start = (state, t,
+    step) at the first timed step of `value`, so both cover the same steps."""
     C = solver.n_cells
+    state, t_start, step_start = start
     pin = [torch.empty(C, dtype=torch.float64).pin_memory() for _ in range(6)]
-    for dst, src in zip(pin[:3], (sc.state.h, sc.state.qx, sc.state.qy)):
+    for dst, src in zip(pin[:3], (state.h, state.qx, state.qy)):
         dst.numpy()[:] = src
     ptrs_in = [p.data_ptr() for p in pin[:3]]
     ptrs_out = [p.data_ptr() for p in pin[3:]]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    solver.set_state_ptrs(*ptrs_in, t=0.0, step=0)
-    recs = solver.advance(t_end=horizon, max_steps=K)
+    solver.set_state_ptrs(*ptrs_in, t=t_start, step=step_start)
+    recs = solver.advance(t_end=horizon, max_steps=step_start + K)
     solver.get_state_ptrs(*ptrs_out)
     el = time.perf_counter() - t0
     assert len(recs) == K
@@ -656,7 +661,8 @@ def e2e_run(api, solver, sc, K, horizon, torch):
     return {"value": C * K / el, "unit": UNIT, "h2d_bytes_per_step": h2d / K,
             "d2h_bytes_per_step": d2h / K, "wall_s": el,
             "path": "swe_dev_set_state (pinned H2D) + swe_dev_advance (K steps, stats rows D2H) + "
-                    "swe_dev_get_state (pinned D2H), host wall clock"}
+                    "swe_dev_get_state (pinned D2H), host wall clock; the same K steps as value "
+                    "(from the state at its first timed step)"}
 
 
 def cpu_baseline(sc, mesh, args):
