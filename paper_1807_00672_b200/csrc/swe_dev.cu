@@ -427,20 +427,21 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
     const double span = std::max(x1 - x0, y1 - y0);
     double* dcx = (double*)tmp.get(sizeof(double) * Co);
     double* dcy = (double*)tmp.get(sizeof(double) * Co);
-    unsigned* kin = (unsigned*)k64a;
-    unsigned* kout = (unsigned*)k64b;
     ok = dcx && dcy && up(dcx, m->cx, sizeof(double) * Co) && up(dcy, m->cy, sizeof(double) * Co);
     if (ok) {
 #if SWE_HILBERT == 2
       const double side = std::max(std::min(x1 - x0, y1 - y0), span / 255.0) * (1.0 + 1e-9);
       k_hilbert_blocks<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
                                                           side > 0 ? side : 1.0,
-                                                          (y1 - y0) > (x1 - x0), kin, idx);
+                                                          (y1 - y0) > (x1 - x0), k64a, idx);
+      ok = radix_sort(tmp, k64a, k64b, idx, c_orig, Co, 40, s);
 #else
+      unsigned* kin = (unsigned*)k64a;
+      unsigned* kout = (unsigned*)k64b;
       k_morton<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
                                                   span > 0 ? 65535.0 / span : 0.0, kin, idx);
-#endif
       ok = radix_sort(tmp, kin, kout, idx, c_orig, Co, 32, s);
+#endif
     }
   }
   if (ok) k_invert<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig, c_new);

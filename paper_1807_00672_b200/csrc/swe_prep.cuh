@@ -62,10 +62,10 @@ __global__ void k_morton(int C, const double* cx, const double* cy, double x0, d
 }
 
 // SWE_HILBERT=2: the bounding box cut into squares along its long axis, each
-// traversed by a 4096^2 Hilbert curve (a curve ends at the corner where the
-// next square's begins); key = square index << 24 | Hilbert index
+// traversed by a 65536^2 Hilbert curve (a curve ends at the corner where the
+// next square's begins); key = square index << 32 | Hilbert index (40 bits)
 __global__ void k_hilbert_blocks(int C, const double* cx, const double* cy, double x0, double y0,
-                                 double side, int long_is_y, unsigned* key, int* idx) {
+                                 double side, int long_is_y, unsigned long long* key, int* idx) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= C) return;
   double a = (cx[c] - x0) / side, b = (cy[c] - y0) / side;
@@ -75,9 +75,9 @@ __global__ void k_hilbert_blocks(int C, const double* cx, const double* cy, doub
     b = t;
   }
   const double blk = fmin(fmax(floor(a), 0.0), 255.0);
-  const double fx = fmin(fmax((a - blk) * 4096.0, 0.0), 4095.0);
-  const double fy = fmin(fmax(b * 4096.0, 0.0), 4095.0);
-  key[c] = ((unsigned)blk << 24) | (hilbert16((unsigned)fx << 4, (unsigned)fy << 4) >> 8);
+  const double fx = fmin(fmax((a - blk) * 65536.0, 0.0), 65535.0);
+  const double fy = fmin(fmax(b * 65536.0, 0.0), 65535.0);
+  key[c] = ((unsigned long long)blk << 32) | hilbert16((unsigned)fx, (unsigned)fy);
   idx[c] = c;
 }
 
