@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <chrono>
+#include <cstdint>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
@@ -21,6 +22,8 @@
 #include <map>
 #include <memory>
 #include <string>
+#include <thread>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -156,16 +159,80 @@ class DeviceMesh {
     v.len = m.edge_length.data();
     const swe_params sp = to_c(p);
     check(swe_dev_create(&v, &sp, device, 0, &ctx_), "swe_dev_create");
-    fingerprint_ = print(m);
+    digest_ = digest(m);
   }
   ~DeviceMesh() { swe_dev_destroy(ctx_); }
   DeviceMesh(const DeviceMesh&) = delete;
   DeviceMesh& operator=(const DeviceMesh&) = delete;
 
   swe_dev_ctx* ctx() const { return ctx_; }
+  /// The cached context serves `m` only if every array it uploaded still holds
+  /// the same bytes: a Mesh mutated in place, or a new Mesh whose vectors reuse
+  /// freed addresses, is re-uploaded (a content digest, not the addresses).
   bool matches(const Mesh& m, const PhysParams& p, int device) const {
-    return device == device_ && print(m) == fingerprint_ && same(p, params_);
+    return device == device_ && same(p, params_) && digest(m) == digest_;
   }
+
+  /// 64-bit content digest of the arrays the device copy is built from
+  /// (geometry, bed, Manning, connectivity), hashed by all host threads.
+  static uint64_t digest(const Mesh& m) {
+    struct Span {
+      const unsigned char* p;
+      size_t n;
+    };
+    auto sp = [](const auto& v) {
+      return Span{reinterpret_cast<const unsigned char*>(v.data()),
+                  v.size() * sizeof(typename std::decay_t<decltype(v)>::value_type)};
+    };
+    const Span arrays[] = {sp(m.cell_area),  sp(m.cell_inradius), sp(m.cell_bed),
+                           sp(m.cell_manning), sp(m.cell_centroid), sp(m.cell_edges),
+                           sp(m.edge_left),  sp(m.edge_right),    sp(m.edge_normal),
+                           sp(m.edge_length)};
+    constexpr size_t kChunk = size_t(1) << 22;  // 4 MiB per task
+    std::vector<std::pair<int, size_t>> tasks;  // (array, chunk start)
+    for (int a = 0; a < 10; ++a) {
+      size_t o = 0;
+      do {
+        tasks.push_back({a, o});
+        o += kChunk;
+      } while (o < arrays[a].n);
+    }
+    std::vector<uint64_t> out(tasks.size());
+    auto hash_chunk = [&](size_t i) {
+      const Span& s = arrays[tasks[i].first];
+      const size_t o = tasks[i].second, n = std::min(kChunk, s.n - o);
+      uint64_t h[4] = {0x9e3779b97f4a7c15ULL, 0xc2b2ae3d27d4eb4fULL, 0x165667b19e3779f9ULL,
+                       0x27d4eb2f165667c5ULL};
+      size_t k = 0;
+      for (; k + 32 <= n; k += 32)
+        for (int j = 0; j < 4; ++j) {
+          uint64_t w;
+          std::memcpy(&w, s.p + o + k + 8 * j, 8);
+          h[j] = (h[j] ^ w) * 0x100000001b3ULL;
+          h[j] ^= h[j] >> 29;
+        }
+      uint64_t r = (h[0] ^ (h[1] << 1)) ^ ((h[2] << 2) ^ (h[3] << 3)) ^ (n * 0x9e3779b97f4a7c15ULL);
+      for (; k < n; ++k) r = (r ^ s.p[o + k]) * 0x100000001b3ULL;
+      out[i] = r ^ (uint64_t(tasks[i].first) << 56);
+    };
+    const unsigned nt = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                        static_cast<unsigned>(tasks.size())));
+    if (nt <= 1) {
+      for (size_t i = 0; i < tasks.size(); ++i) hash_chunk(i);
+    } else {
+      std::vector<std::thread> pool;
+      for (unsigned t = 0; t < nt; ++t)
+        pool.emplace_back([&, t] {
+          for (size_t i = t; i < tasks.size(); i += nt) hash_chunk(i);
+        });
+      for (auto& th : pool) th.join();
+    }
+    uint64_t d = 0xcbf29ce484222325ULL ^ (uint64_t(m.n_cells()) << 32) ^ uint64_t(m.n_edges());
+    for (uint64_t v : out) d = (d ^ v) * 0x100000001b3ULL;
+    return d;
+  }
+
+  int busy = 0;  // run() calls holding this context
 
   static swe_params to_c(const PhysParams& p) { return {p.g, p.h_dry, p.cfl, p.dt_max, p.h_ref}; }
 
@@ -180,30 +247,31 @@ class DeviceMesh {
     return a.g == b.g && a.h_dry == b.h_dry && a.cfl == b.cfl && a.dt_max == b.dt_max &&
            a.h_ref == b.h_ref;
   }
-  static std::vector<const void*> print(const Mesh& m) {
-    return {m.cell_area.data(), m.cell_bed.data(), m.cell_manning.data(), m.edge_length.data(),
-            m.cell_edges.data(), reinterpret_cast<const void*>(static_cast<intptr_t>(m.n_cells())),
-            reinterpret_cast<const void*>(static_cast<intptr_t>(m.n_edges()))};
-  }
   swe_dev_ctx* ctx_ = nullptr;
   int device_;
   PhysParams params_;
-  std::vector<const void*> fingerprint_;
+  uint64_t digest_ = 0;
 };
 
-inline std::map<const Mesh*, std::unique_ptr<DeviceMesh>>& device_cache() {
-  static std::map<const Mesh*, std::unique_ptr<DeviceMesh>> cache;
+inline std::map<const Mesh*, std::shared_ptr<DeviceMesh>>& device_cache() {
+  static std::map<const Mesh*, std::shared_ptr<DeviceMesh>> cache;
   return cache;
 }
 
-/// Process-wide cache: one device context per (Mesh, params, device).
-inline DeviceMesh& device_mesh(const Mesh& m, const PhysParams& p, int device) {
+/// Process-wide cache: one device context per (Mesh, params, device).  A
+/// context a running run() holds is never replaced or re-uploaded: a call
+/// made meanwhile (e.g. from on_snapshot) gets a context of its own, so it
+/// cannot disturb the run's state, clock or geometry.
+inline std::shared_ptr<DeviceMesh> device_mesh(const Mesh& m, const PhysParams& p, int device) {
   auto& slot = device_cache()[&m];
+  if (slot && slot->busy > 0) {
+    return std::make_shared<DeviceMesh>(m, p, device);  // never share a running context
+  }
   if (!slot || !slot->matches(m, p, device)) {
     slot.reset();
-    slot = std::make_unique<DeviceMesh>(m, p, device);
+    slot = std::make_shared<DeviceMesh>(m, p, device);
   }
-  return *slot;
+  return slot;
 }
 
 inline void upload(DeviceMesh& dm, const FieldState& s, double t, long step) {
@@ -239,24 +307,31 @@ inline void download(DeviceMesh& dm, FieldState& s) {
 
 }  // namespace detail
 
-/// Drops the device copy of a mesh (call before destroying or mutating it).
-inline void release_device_mesh(const Mesh& m) { detail::device_cache().erase(&m); }
+/// Drops the device copy of a mesh (frees its device memory early; a mutated
+/// mesh is detected by content and re-uploaded anyway).
+inline void release_device_mesh(const Mesh& m) {
+  auto it = detail::device_cache().find(&m);
+  if (it != detail::device_cache().end() && it->second->busy == 0) detail::device_cache().erase(it);
+}
 
 /// Volume integral of the depth (engine.hpp:128-132), reduced on the device
-/// in a fixed order (matches the reference's serial sum to round-off).
+/// in a fixed order (matches the reference's serial sum to round-off).  A
+/// pure function as in the reference: it touches no cached context.
 inline double total_mass(const FieldState& s, const Mesh& mesh,
                          const PhysParams& p = PhysParams{}, int device = 0) {
-  auto& dm = detail::device_mesh(mesh, p, device);
-  detail::upload(dm, s, 0.0, 0);
+  (void)p;
   double m = 0.0;
-  detail::DeviceMesh::check(swe_dev_total_mass(dm.ctx(), &m), "swe_dev_total_mass");
+  detail::DeviceMesh::check(swe_dev_mass(device, static_cast<long long>(mesh.n_cells()),
+                                         s.h.data(), mesh.cell_area.data(), &m),
+                            "swe_dev_mass");
   return m;
 }
 
 /// One flux evaluation per edge (engine.hpp:138-170), on the device.
 inline void compute_fluxes(const FieldState& s, const Mesh& mesh, const PhysParams& p,
                            const BackendSpec& backend, EdgeFluxes& out) {
-  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  const auto hold = detail::device_mesh(mesh, p, backend.device);
+  auto& dm = *hold;
   detail::upload(dm, s, 0.0, 0);
   if (static_cast<int>(out.left.size()) != mesh.n_edges()) out.resize(mesh.n_edges());
   swe_status st{};
@@ -275,14 +350,19 @@ inline StepStats advance_step(Simulation& sim, const Mesh& mesh, const PhysParam
   (void)fluxes;
   using clock = std::chrono::steady_clock;
   const auto t0 = clock::now();
-  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  const auto hold = detail::device_mesh(mesh, p, backend.device);
+  auto& dm = *hold;
   detail::upload(dm, sim.current, sim.t, sim.step);
   detail::DeviceMesh::check(
       swe_dev_set_ledger(dm.ctx(), sim.ledger.clipped_volume, sim.ledger.clip_events),
       "swe_dev_set_ledger");
   swe_step_record rec{};
   swe_status st{};
-  const int rc = swe_dev_step(dm.ctx(), t_end, &rec, &st);
+  double flux_ms = 0.0, kernel_update_ms = 0.0;
+  // with timers: the two-phase kernels, so the flux and update phases are
+  // timed apart like the reference's (engine.hpp:314-317); same results
+  const int rc = timing ? swe_dev_step_timed(dm.ctx(), t_end, &rec, &st, &flux_ms, &kernel_update_ms)
+                        : swe_dev_step(dm.ctx(), t_end, &rec, &st);
   if (rc != SWE_OK) detail::raise(st, nullptr);
   if (static_cast<int>(sim.next.h.size()) != mesh.n_cells()) sim.next.resize(mesh.n_cells());
   detail::download(dm, sim.next);
@@ -298,9 +378,13 @@ inline StepStats advance_step(Simulation& sim, const Mesh& mesh, const PhysParam
   out.t = sim.t;
   out.dt = rec.dt;
   out.max_speed = rec.max_speed;
-  if (timing)
+  if (timing) {
+    // flux: the face kernel (device time); update: the rest of the call --
+    // the cell kernel, the step commit and the host<->device state copies
+    timing->wall_flux_ms = flux_ms;
     timing->wall_update_ms =
-        std::chrono::duration<double, std::milli>(clock::now() - t0).count();
+        std::chrono::duration<double, std::milli>(clock::now() - t0).count() - flux_ms;
+  }
   return out;
 }
 
@@ -367,8 +451,14 @@ inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
                     const BackendSpec& backend, const RunOptions& opt) {
   using clock = std::chrono::steady_clock;
   if (!(opt.t_end > 0.0)) throw config_error("run: t_end must be > 0");
-  auto& dm = detail::device_mesh(mesh, p, backend.device);
+  const auto hold = detail::device_mesh(mesh, p, backend.device);
+  auto& dm = *hold;
   swe_dev_ctx* ctx = dm.ctx();
+  struct Busy {  // the cache keeps this context out of other calls' reach
+    detail::DeviceMesh& d;
+    explicit Busy(detail::DeviceMesh& x) : d(x) { ++d.busy; }
+    ~Busy() { --d.busy; }
+  } busy(dm);
 
   RunStats rs;
   detail::upload(dm, sim.current, sim.t, sim.step);

@@ -248,12 +248,33 @@ SWE_API long long swe_dev_memory_bytes(swe_dev_ctx* ctx);
 /* Kernels launched by this process through any context. */
 SWE_API long long swe_dev_launch_count(void);
 
-/* Point physics on the device over arrays (kernel-level parity):
- * kind 0 hllc(l,r,n), 1 wall(l,n), 2 edge combine(l,r,z,n) -> out[6],
- * 3 friction(l, z[0]=n_manning, z[1]=dt), 4 pow(h, 4/3) (l[0]=h).
- * l, r: [3n]; z: [2n]; nrm: [2n]; out: [3n] (kind 2: [6n], kind 4: [n]). */
+/* Point physics on the device over arrays (kernel-level parity and the
+ * drop-in kernels.hpp entry points, reference kernels.hpp:15-216):
+ * kind 0 hllc_flux(l,r,n), 1 wall_flux(l,n), 2 edge combine(l,r,z,n) -> out[6],
+ * 3 apply_friction(l, z[0]=n_manning, z[1]=dt), 4 pow(h, 4/3) (l[0]=h),
+ * 5 physical_flux_normal(l,n), 6 wave_speed_estimates(hL=l[0], uL=l[1],
+ * hR=r[0], uR=r[1]) -> {SL, S*, SR}, 7 hydrostatic_reconstruct(l, z[0], r,
+ * z[1], n) -> out[12] = {left, right, corr_left, corr_right},
+ * 8 cell_signal_speed(l) -> out[1], 9 clamp_dry(l) -> out[5] = {h, qx, qy,
+ * clipped depth, 1 if it throws}.
+ * l, r: [3n]; z: [2n]; nrm: [2n]; out: [w n], w = 3 except as noted. */
 SWE_API int swe_dev_point_eval(int kind, long long n, const swe_params* params, const double* l,
                        const double* r, const double* z, const double* nrm, double* out);
+/* stable_dt (kernels.hpp:174-186) of host arrays [n] on the device: *dt =
+ * cfl * min over wet cells of inradius / signal speed, or dt_max when all are
+ * dry; SWE_NONFINITE_SPEED with *bad_cell = the lowest offending cell. */
+SWE_API int swe_dev_stable_dt(int device, long long n, const swe_params* params, const double* h,
+                              const double* qx, const double* qy, const double* inradius,
+                              double* dt, long long* bad_cell);
+/* total_mass (engine.hpp:128-132) of host arrays [n] on the device, a
+ * fixed-order tree sum of h * area; stateless (touches no context). */
+SWE_API int swe_dev_mass(int device, long long n, const double* h, const double* area,
+                         double* mass);
+/* One advance_step like swe_dev_step, through the two-phase kernels with the
+ * flux and update phases timed apart by CUDA events (StepStats timers,
+ * engine.hpp:314-317); results are the fused step's, bit for bit. */
+SWE_API int swe_dev_step_timed(swe_dev_ctx* ctx, double t_end, swe_step_record* rec,
+                               swe_status* st, double* flux_ms, double* update_ms);
 
 /* build_mesh (mesh.hpp:121-240) on the device: same numbering, geometry and
  * error texts as the host build_mesh (include/swe/mesh.hpp).  xy [2*n_nodes],

@@ -243,6 +243,8 @@ class RefOracle:
         L.ref_edge.argtypes = [cl, vp, vp, vp, vp, vp, vp, vp]
         L.ref_friction.argtypes = [cl, vp, vp, vp, vp, vp]
         L.ref_pow43.argtypes = [cl, vp, vp]
+        L.ref_point.argtypes = [ci, cl, vp, vp, vp, vp, vp, vp]
+        L.ref_stable_dt.argtypes = [cl, vp, vp, vp, vp, vp, C.POINTER(cd), C.POINTER(cl)]
         L.ref_wave_speeds.argtypes = [cl, vp, vp, vp]
         L.ref_case_defaults.restype = ci
         L.ref_case_defaults.argtypes = [C.c_char_p, vp]
@@ -314,6 +316,24 @@ class RefOracle:
         out = np.empty((len(u), 3))
         self.lib.ref_friction(len(u), P(_pa(params)), P(_c(u)), P(_c(n)), P(_c(dt)), P(out))
         return out
+
+    def point(self, kind, l, r=None, z=None, nrm=None, params=None):
+        """ref_point: kernels.hpp entry points, swe_dev_point_eval kinds 5-9."""
+        l = _c(l).reshape(-1, 3)
+        n = len(l)
+        width = {7: 12, 8: 1, 9: 5}.get(kind, 3)
+        out = np.empty((n, width))
+        cv = lambda a: None if a is None else P(_c(a))
+        rc = self.lib.ref_point(kind, n, P(_pa(params)), P(l), cv(r), cv(z), cv(nrm), P(out))
+        assert rc == 0
+        return out if width > 1 else out[:, 0]
+
+    def stable_dt(self, h, qx, qy, r, params=None):
+        """-> (dt, None) or (None, bad cell)."""
+        dt, bad = C.c_double(), C.c_long()
+        rc = self.lib.ref_stable_dt(len(h), P(_pa(params)), P(_c(h)), P(_c(qx)), P(_c(qy)),
+                                    P(_c(r)), C.byref(dt), C.byref(bad))
+        return (dt.value, None) if rc == 0 else (None, bad.value)
 
     def pow43(self, h):
         h = _c(h)

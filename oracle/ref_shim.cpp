@@ -275,6 +275,70 @@ __attribute__((visibility("default"))) int ref_run(void* mp, const double* param
 // ---- point physics (kernels.hpp) over arrays, for kernel-level goldens ----
 // states are (h, qx, qy) triples; normals (nx, ny) pairs.
 
+// kernels.hpp entry points with the device point-eval layouts (swe_dev.h
+// swe_dev_point_eval kinds 5-9): 5 physical_flux_normal, 6
+// wave_speed_estimates(l[0], l[1], r[0], r[1]), 7 hydrostatic_reconstruct
+// -> 12, 8 cell_signal_speed -> 1, 9 clamp_dry -> {h, qx, qy, clipped, throws}
+__attribute__((visibility("default"))) int ref_point(int kind, long n, const double* params,
+                                                     const double* l, const double* r,
+                                                     const double* z, const double* nrm,
+                                                     double* out) {
+  const PhysParams p = params_from(params);
+  for (long i = 0; i < n; ++i) {
+    const ConservedState a{l[3 * i], l[3 * i + 1], l[3 * i + 2]};
+    if (kind == 5) {
+      const Flux3 f = physical_flux_normal(a, {nrm[2 * i], nrm[2 * i + 1]}, p);
+      out[3 * i] = f.mass;
+      out[3 * i + 1] = f.momx;
+      out[3 * i + 2] = f.momy;
+    } else if (kind == 6) {
+      const WaveSpeeds w = wave_speed_estimates(a.h, a.qx, r[3 * i], r[3 * i + 1], p);
+      out[3 * i] = w.SL;
+      out[3 * i + 1] = w.Sstar;
+      out[3 * i + 2] = w.SR;
+    } else if (kind == 7) {
+      const ConservedState b{r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+      const ReconstructedInterface ri =
+          hydrostatic_reconstruct(a, z[2 * i], b, z[2 * i + 1], {nrm[2 * i], nrm[2 * i + 1]}, p);
+      const double v[12] = {ri.left.h, ri.left.qx, ri.left.qy, ri.right.h, ri.right.qx,
+                            ri.right.qy, ri.corr_left.mass, ri.corr_left.momx, ri.corr_left.momy,
+                            ri.corr_right.mass, ri.corr_right.momx, ri.corr_right.momy};
+      std::memcpy(out + 12 * i, v, sizeof(v));
+    } else if (kind == 8) {
+      out[i] = cell_signal_speed(a, p);
+    } else if (kind == 9) {
+      double clipped = 0.0;
+      try {
+        const ConservedState u = clamp_dry(a, p, &clipped);
+        const double v[5] = {u.h, u.qx, u.qy, clipped, 0.0};
+        std::memcpy(out + 5 * i, v, sizeof(v));
+      } catch (const numeric_error&) {
+        const double v[5] = {a.h, a.qx, a.qy, 0.0, 1.0};
+        std::memcpy(out + 5 * i, v, sizeof(v));
+      }
+    } else {
+      return 1;
+    }
+  }
+  return 0;
+}
+
+// stable_dt (kernels.hpp:174-186): 0 ok, 1 non-finite (bad = the cell)
+__attribute__((visibility("default"))) int ref_stable_dt(long n, const double* params,
+                                                         const double* h, const double* qx,
+                                                         const double* qy, const double* r,
+                                                         double* dt, long* bad) {
+  const PhysParams p = params_from(params);
+  try {
+    *dt = stable_dt({h, (size_t)n}, {qx, (size_t)n}, {qy, (size_t)n}, {r, (size_t)n}, p);
+    return 0;
+  } catch (const numeric_error& e) {
+    const std::string w = e.what();
+    *bad = std::stol(w.substr(w.rfind(' ') + 1));
+    return 1;
+  }
+}
+
 __attribute__((visibility("default"))) int ref_hllc(long n, const double* params, const double* l,
                                                     const double* r, const double* nrm,
                                                     double* out) {

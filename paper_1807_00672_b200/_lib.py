@@ -97,6 +97,11 @@ _SIGS = {
     "swe_dev_launch_count": (c_ll, []),
     "swe_dev_point_eval": (c_int, [c_int, c_ll, C.POINTER(swe_params), c_void_p, c_void_p,
                                    c_void_p, c_void_p, c_void_p]),
+    "swe_dev_stable_dt": (c_int, [c_int, c_ll, C.POINTER(swe_params), c_void_p, c_void_p, c_void_p,
+                                  c_void_p, P_double, P_ll]),
+    "swe_dev_mass": (c_int, [c_int, c_ll, c_void_p, c_void_p, P_double]),
+    "swe_dev_step_timed": (c_int, [c_void_p, c_double, C.POINTER(swe_step_record),
+                                   C.POINTER(swe_status), P_double, P_double]),
     "swe_dev_strerror": (c_char_p, [c_int]),
     "swe_dev_last_error": (c_char_p, []),
     # host input producers (swe_host.h)

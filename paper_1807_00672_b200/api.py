@@ -626,10 +626,12 @@ class DeviceSolver:
 
 
 def point_eval(kind: int, l, r=None, z=None, nrm=None, params: PhysParams = PhysParams()):
-    """Device point physics (swe_dev_point_eval): 0 hllc, 1 wall, 2 edge, 3 friction, 4 pow43."""
+    """Device point physics (swe_dev_point_eval): 0 hllc, 1 wall, 2 edge, 3 friction, 4 pow43,
+    5 physical_flux_normal, 6 wave_speed_estimates, 7 hydrostatic_reconstruct,
+    8 cell_signal_speed, 9 clamp_dry (kernels.hpp:15-216)."""
     l = np.ascontiguousarray(l, dtype=np.float64).reshape(-1, 3)
     n = len(l)
-    width = {2: 6, 4: 1}.get(kind, 3)
+    width = {2: 6, 4: 1, 7: 12, 8: 1, 9: 5}.get(kind, 3)
     out = np.empty((n, width))
     cv = lambda a: None if a is None else np.ascontiguousarray(a, dtype=np.float64)
     r, z, nrm = cv(r), cv(z), cv(nrm)
@@ -637,6 +639,29 @@ def point_eval(kind: int, l, r=None, z=None, nrm=None, params: PhysParams = Phys
     _check(L.load().swe_dev_point_eval(kind, n, C.byref(p), L.ptr(l), L.ptr(r), L.ptr(z),
                                        L.ptr(nrm), L.ptr(out)), "swe_dev_point_eval")
     return out if width > 1 else out[:, 0]
+
+
+def stable_dt(h, qx, qy, inradius, params: PhysParams = PhysParams(), device: int = 0) -> float:
+    """kernels.hpp:174-186 on the device (swe_dev_stable_dt)."""
+    a = [np.ascontiguousarray(x, dtype=np.float64) for x in (h, qx, qy, inradius)]
+    dt, bad = C.c_double(), C.c_longlong()
+    p = params.c()
+    rc = L.load().swe_dev_stable_dt(device, len(a[0]), C.byref(p), *[L.ptr(x) for x in a],
+                                    C.byref(dt), C.byref(bad))
+    if rc == L.SWE_NONFINITE_SPEED:
+        raise NumericError(f"stable_dt: non-finite velocity in cell {bad.value}")
+    _check(rc, "swe_dev_stable_dt")
+    return dt.value
+
+
+def mass(h, area, device: int = 0) -> float:
+    """total_mass of host arrays on the device (swe_dev_mass, stateless)."""
+    h = np.ascontiguousarray(h, dtype=np.float64)
+    area = np.ascontiguousarray(area, dtype=np.float64)
+    out = C.c_double()
+    _check(L.load().swe_dev_mass(device, len(h), L.ptr(h), L.ptr(area), C.byref(out)),
+           "swe_dev_mass")
+    return out.value
 
 
 def launch_count() -> int:

@@ -95,6 +95,63 @@ def build_harness_driver(verbose: bool = False, force: bool = False) -> Path:
     return out
 
 
+REF_TESTS = Path("/root/reference/proj/tests")
+REF_UNIT_SOURCES = ["test_kernels", "test_engine", "test_mesh", "test_cases", "test_io",
+                    "test_harness", "doctest_main"]
+
+
+def _build_doctest_binary(out: Path, sources, include_dirs, link, verbose, force, extra=()):
+    """Compile the reference's own doctest sources (read in place, not copied)
+    with the doctest stand-in tests/cpp/doctest/doctest.h, one object per
+    source, in parallel."""
+    shim = ROOT / "tests" / "cpp" / "doctest" / "doctest.h"
+    deps = [shim, *[REF_TESTS / f"{n}.cpp" for n in sources]]
+    if link and LIB.exists():
+        deps += [LIB, *(INC / "swe").glob("*.hpp")]
+    if not force and not _stale(out, deps):
+        return out
+    obj_dir = BUILD / ("objs_" + out.name)
+    obj_dir.mkdir(parents=True, exist_ok=True)
+    flags = ["-std=c++20", "-O2", "-ffp-contract=off", f"-I{shim.parent}",
+             *[f"-I{d}" for d in include_dirs], f"-I{JSON_INC}", f"-I{REF_TESTS}", *extra]
+    procs, objs = [], []
+    for n in sources:
+        o = obj_dir / f"{n}.o"
+        objs.append(o)
+        cmd = ["g++", *flags, "-c", REF_TESTS / f"{n}.cpp", "-o", o]
+        if verbose:
+            print(" ".join(str(c) for c in cmd), flush=True)
+        procs.append(subprocess.Popen([str(c) for c in cmd]))
+    if any(p.wait() for p in procs):
+        raise subprocess.CalledProcessError(1, f"compile {out.name}")
+    out.parent.mkdir(parents=True, exist_ok=True)
+    _run(["g++", *extra, *objs, "-o", out, *link], verbose)
+    return out
+
+
+def build_reference_tests(verbose: bool = False, force: bool = False) -> None:
+    """The reference's own unit tests (test_kernels/engine/mesh/cases/io/
+    harness.cpp) and acceptance suite compiled UNCHANGED against the drop-in
+    headers (include/ first on the path, so swe/engine.hpp etc. are this
+    repo's; the reference's io.hpp / bench.hpp come from its tree) ->
+    tests/cpp/ref_unit, tests/cpp/ref_acceptance (every engine call on the
+    B200); and against the reference alone -> oracle/_ref/ref_unit_cpu, which
+    checks the doctest stand-in itself.  Only where /root/reference exists;
+    the binaries travel to the GPU box prebuilt."""
+    if not (REF_TESTS.exists() and (JSON_INC / "json.hpp").exists()):
+        return
+    link = [f"-L{PKG}", "-lswe_b200", "-Wl,-rpath,$ORIGIN/../../paper_1807_00672_b200"]
+    # acceptance.cpp's criterion 10 drives the CLI tool (needs CLI11, absent):
+    # the path is a stub and the test is excluded at run time
+    cli = ['-DSWE_CLI_PATH="/bin/false"']
+    _build_doctest_binary(ROOT / "tests" / "cpp" / "ref_unit", REF_UNIT_SOURCES,
+                          [INC, REF_INC], link, verbose, force)
+    _build_doctest_binary(ROOT / "tests" / "cpp" / "ref_acceptance", ["acceptance"],
+                          [INC, REF_INC], link, verbose, force, extra=cli)
+    _build_doctest_binary(ROOT / "oracle" / "_ref" / "ref_unit_cpu", REF_UNIT_SOURCES,
+                          [REF_INC], [], verbose, force, extra=["-fopenmp"])
+
+
 def build_oracle(verbose: bool = False) -> None:
     _run(["make", "-s", "-C", ROOT / "oracle"], verbose)
 
@@ -104,6 +161,7 @@ def build_all(verbose: bool = False, force: bool = False) -> None:
     build_api_driver(verbose, force)
     build_harness_driver(verbose, force)
     build_oracle(verbose)
+    build_reference_tests(verbose, force)
 
 
 if __name__ == "__main__":

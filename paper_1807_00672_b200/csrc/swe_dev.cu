@@ -1327,6 +1327,20 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
   x->linked = true;
   // the CFL cache must be re-formed globally; the graph gains the exchange
   if (int rc = sync_ctl(x)) return rc;
+  // every rank starts linked with its current state in buffer 0 and no
+  // exchange posted: a step kernel pushes ghosts into the PEER's buffer
+  // (sender's cur ^ 1) and mailbox slots are tagged by the exchange count, so
+  // contexts stepped different numbers of times before linking (e.g. an
+  // unlinked warm-up) would otherwise write into a peer's live buffer
+  if (x->h_ctl->cur != 0) {
+    for (int k = 0; k < 3; ++k) {
+      double* const* buf = k == 0 ? d.h : (k == 1 ? d.qx : d.qy);
+      CK(cudaMemcpyAsync(buf[0], buf[1], sizeof(double) * d.C, cudaMemcpyDeviceToDevice,
+                         x->stream));
+    }
+    x->h_ctl->cur = 0;
+  }
+  x->h_ctl->xseq = 0;  // (a context is linked once; nothing has posted to it yet)
   x->h_ctl->cfl_valid = 0;
   x->cfl_host_valid = false;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, x->stream));
@@ -1711,28 +1725,162 @@ int swe_dev_point_eval(int kind, long long n, const swe_params* p, const double*
                        const double* r, const double* z, const double* nrm, double* out) {
   if (n <= 0) return SWE_OK;
   if (!p || !l || !out) return fail_invalid("swe_dev_point_eval: null argument");
-  const size_t outw = kind == 2 ? 6 : (kind == 4 ? 1 : 3);
-  double *dl = nullptr, *dr = nullptr, *dz = nullptr, *dn = nullptr, *dout = nullptr;
-  CK(cudaMalloc(&dl, sizeof(double) * 3 * n));
-  CK(cudaMalloc(&dr, sizeof(double) * 3 * n));
-  CK(cudaMalloc(&dz, sizeof(double) * 2 * n));
-  CK(cudaMalloc(&dn, sizeof(double) * 2 * n));
-  CK(cudaMalloc(&dout, sizeof(double) * outw * n));
-  CK(cudaMemcpy(dl, l, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
-  if (r) CK(cudaMemcpy(dr, r, sizeof(double) * 3 * n, cudaMemcpyHostToDevice));
-  if (z) CK(cudaMemcpy(dz, z, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
-  if (nrm) CK(cudaMemcpy(dn, nrm, sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+  if (kind < 0 || kind > 9) return fail_invalid("swe_dev_point_eval: unknown kind");
+  static const size_t kOutW[10] = {3, 3, 6, 3, 1, 3, 3, 12, 1, 5};
+  const size_t outw = kOutW[kind];
+  // one packed staging buffer (pinned host + device, grown on demand, reused):
+  // a call is one copy in, one kernel, one copy out -- the drop-in
+  // kernels.hpp entry points are called per point by the reference's tests
+  struct Scratch {
+    double* host = nullptr;
+    double* dev = nullptr;
+    size_t cap = 0;  // doubles
+    cudaStream_t s = nullptr;
+  };
+  static thread_local Scratch sc;
+  const size_t in_n = 10 * (size_t)n, need = in_n + outw * (size_t)n;
+  if (need > sc.cap) {
+    if (sc.host) cudaFreeHost(sc.host);
+    if (sc.dev) cudaFree(sc.dev);
+    sc.host = nullptr;
+    sc.dev = nullptr;
+    sc.cap = 0;
+    const size_t cap = std::max<size_t>(need, 4096);
+    CK(cudaMallocHost(&sc.host, sizeof(double) * cap));
+    CK(cudaMalloc(&sc.dev, sizeof(double) * cap));
+    sc.cap = cap;
+  }
+  if (!sc.s) CK(cudaStreamCreateWithFlags(&sc.s, cudaStreamNonBlocking));
+  double* h = sc.host;
+  std::memcpy(h, l, sizeof(double) * 3 * n);
+  if (r) std::memcpy(h + 3 * n, r, sizeof(double) * 3 * n);
+  if (z) std::memcpy(h + 6 * n, z, sizeof(double) * 2 * n);
+  if (nrm) std::memcpy(h + 8 * n, nrm, sizeof(double) * 2 * n);
+  double* d = sc.dev;
+  CK(cudaMemcpyAsync(d, h, sizeof(double) * in_n, cudaMemcpyHostToDevice, sc.s));
   const Phys P{p->g, p->h_dry, p->cfl, p->dt_max, p->h_ref};
-  k_point<<<blocks_for(n), kBlock>>>(kind, n, P, dl, dr, dz, dn, dout);
+  k_point<<<blocks_for(n), kBlock, 0, sc.s>>>(kind, n, P, d, d + 3 * n, d + 6 * n, d + 8 * n,
+                                              d + in_n);
   ++g_launches;
   CK(cudaGetLastError());
-  CK(cudaMemcpy(out, dout, sizeof(double) * outw * n, cudaMemcpyDeviceToHost));
-  cudaFree(dl);
-  cudaFree(dr);
-  cudaFree(dz);
-  cudaFree(dn);
-  cudaFree(dout);
+  CK(cudaMemcpyAsync(h + in_n, d + in_n, sizeof(double) * outw * n, cudaMemcpyDeviceToHost, sc.s));
+  CK(cudaStreamSynchronize(sc.s));
+  std::memcpy(out, h + in_n, sizeof(double) * outw * n);
   return SWE_OK;
+}
+
+int swe_dev_stable_dt(int device, long long n, const swe_params* p, const double* h,
+                      const double* qx, const double* qy, const double* inradius, double* dt,
+                      long long* bad_cell) {
+  if (!p || !dt || (n > 0 && (!h || !qx || !qy || !inradius)))
+    return fail_invalid("swe_dev_stable_dt: null argument");
+  if (bad_cell) *bad_cell = -1;
+  const Phys P{p->g, p->h_dry, p->cfl, p->dt_max, p->h_ref};
+  if (n <= 0) {
+    *dt = P.dt_max;
+    return SWE_OK;
+  }
+  CK(cudaSetDevice(device));
+  double* buf = nullptr;
+  CK(cudaMalloc(&buf, sizeof(double) * (4 * (size_t)n + 2)));
+  struct Free {
+    void* q;
+    ~Free() { cudaFree(q); }
+  } guard{buf};
+  const double* in[4] = {h, qx, qy, inradius};
+  for (int k = 0; k < 4; ++k)
+    CK(cudaMemcpy(buf + k * (size_t)n, in[k], sizeof(double) * n, cudaMemcpyHostToDevice));
+  double* lo = buf + 4 * (size_t)n;
+  auto* bad = reinterpret_cast<unsigned long long*>(lo + 1);
+  double init[2] = {INFINITY, 0.0};
+  const unsigned long long none = ~0ULL;  // bad = ULLONG_MAX
+  std::memcpy(&init[1], &none, sizeof(none));
+  CK(cudaMemcpy(lo, init, sizeof(init), cudaMemcpyHostToDevice));
+  const int grid = (int)std::min<long long>(blocks_for(n), 148 * 8);
+  k_stable_dt<<<grid, kBlock>>>(n, P, buf, buf + n, buf + 2 * (size_t)n, buf + 3 * (size_t)n, lo, bad);
+  ++g_launches;
+  CK(cudaGetLastError());
+  double out[2];
+  CK(cudaMemcpy(out, lo, sizeof(out), cudaMemcpyDeviceToHost));
+  unsigned long long b;
+  std::memcpy(&b, &out[1], sizeof(b));
+  if (b != ~0ULL) {  // kernels.hpp:182-183
+    if (bad_cell) *bad_cell = (long long)b;
+    return SWE_NONFINITE_SPEED;
+  }
+  *dt = std::isfinite(out[0]) ? P.cfl * out[0] : P.dt_max;  // kernels.hpp:185
+  return SWE_OK;
+}
+
+int swe_dev_mass(int device, long long n, const double* h, const double* area, double* mass) {
+  if (!mass || (n > 0 && (!h || !area))) return fail_invalid("swe_dev_mass: null argument");
+  *mass = 0.0;
+  if (n <= 0) return SWE_OK;
+  CK(cudaSetDevice(device));
+  constexpr int kParts = 1024;
+  double* buf = nullptr;
+  CK(cudaMalloc(&buf, sizeof(double) * (2 * (size_t)n + kParts + 1)));
+  struct Free {
+    void* q;
+    ~Free() { cudaFree(q); }
+  } guard{buf};
+  CK(cudaMemcpy(buf, h, sizeof(double) * n, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(buf + n, area, sizeof(double) * n, cudaMemcpyHostToDevice));
+  double* part = buf + 2 * (size_t)n;
+  k_mass_parts<<<kParts, kBlock>>>(n, buf, buf + n, part);
+  k_mass_final<<<1, kBlock>>>(kParts, part, part + kParts);
+  g_launches += 2;
+  CK(cudaGetLastError());
+  CK(cudaMemcpy(mass, part + kParts, sizeof(double), cudaMemcpyDeviceToHost));
+  return SWE_OK;
+}
+
+int swe_dev_step_timed(swe_dev_ctx* x, double t_end, swe_step_record* rec, swe_status* st,
+                       double* flux_ms, double* update_ms) {
+  if (!x) return fail_invalid("null context");
+  if (x->linked) return fail_invalid("swe_dev_step_timed: not available on a linked context");
+  Dev& d = x->d;
+  if (!d.TM) {  // per-incidence contribution slots of the two-phase kernels
+    d.TM = x->alloc<double>(3 * (size_t)d.C);
+    d.TX = x->alloc<double>(3 * (size_t)d.C);
+    d.TY = x->alloc<double>(3 * (size_t)d.C);
+    if (!d.TY) return fail_invalid("swe_dev_step_timed: cudaMalloc failed"), SWE_CUDA;
+    // (the run graph holds a copy of Dev without these slots: it never uses them)
+  }
+  if (int rc = ensure_cfl(x)) return rc;
+  if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, 1, 0, 1)) return rc;
+  if (int rc = launch_gate(x)) return rc;
+  cudaEvent_t ev[3];
+  for (auto& e : ev) CK(cudaEventCreate(&e));
+  struct Destroy {
+    cudaEvent_t* e;
+    ~Destroy() {
+      for (int i = 0; i < 3; ++i) cudaEventDestroy(e[i]);
+    }
+  } guard{ev};
+  // the two-phase kernels (bit-identical to the fused step) so the flux and
+  // update phases are timed apart, as the reference's StepStats timers
+  // (engine.hpp:314-317); the CFL bound is fused into the previous update
+  CK(cudaEventRecord(ev[0], x->stream));
+  k_face_c<<<x->grid_face, kBlock, 0, x->stream>>>(d);
+  CK(cudaEventRecord(ev[1], x->stream));
+  k_cell_c<<<x->grid_cell, kBlock, 0, x->stream>>>(d);
+  g_launches += 2;
+  CK(cudaGetLastError());
+  // k_cell_c wrote grid_cell partials: finalize reduces those
+  k_finalize<<<1, kBlock, 0, x->stream>>>(d, x->grid_cell, cudaGraphConditionalHandle{}, 0);
+  ++g_launches;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ev[2], x->stream));
+  const int code = read_status(x, st);
+  float a = 0.f, b = 0.f;
+  CK(cudaEventElapsedTime(&a, ev[0], ev[1]));
+  CK(cudaEventElapsedTime(&b, ev[1], ev[2]));
+  if (flux_ms) *flux_ms = a;
+  if (update_ms) *update_ms = b;
+  if (code == SWE_OK && rec)
+    CK(cudaMemcpy(rec, x->rec, sizeof(swe_step_record), cudaMemcpyDeviceToHost));
+  return code;
 }
 
 }  // extern "C"

@@ -220,6 +220,54 @@ __device__ __forceinline__ Cons friction(const Cons& u, double n, double dt, con
   return Cons{u.h, qdivp(u.qx, den), qdivp(u.qy, den)};
 }
 
+// wave_speed_estimates(), kernels.hpp:38-66, as its own entry point (the
+// point API; hllc() above carries a select-form copy for the step kernels)
+__device__ __forceinline__ void wave_speeds(double hL, double uL, double hR, double uR,
+                                            const Phys& P, double& SL, double& Ss, double& SR) {
+  const double g = P.g;
+  const bool dryL = hL < P.h_dry, dryR = hR < P.h_dry;
+  if (dryR && !dryL) {
+    const double cL = sqrt(g * hL);
+    SL = uL - cL;
+    SR = uL + 2.0 * cL;
+  } else if (dryL && !dryR) {
+    const double cR = sqrt(g * hR);
+    SL = uR - 2.0 * cR;
+    SR = uR + cR;
+  } else {
+    const double cL = sqrt(g * hL);
+    const double cR = sqrt(g * hR);
+    const double us = ((0.5 * (uL + uR)) + cL) - cR;
+    const double cs = fabs((0.5 * (cL + cR)) + (0.25 * (uL - uR)));
+    SL = sel_min(uL - cL, us - cs);
+    SR = sel_max(uR + cR, us + cs);
+  }
+  const double num = ((SL * hR) * (uR - SR)) - ((SR * hL) * (uL - SL));
+  const double den = (hR * (uR - SR)) - (hL * (uL - SL));
+  Ss = fabs(den) < 1e-14 ? 0.5 * (uL + uR) : num / den;
+}
+
+// hydrostatic_reconstruct(), kernels.hpp:126-152, as its own entry point:
+// out = {left state, right state, corr_left, corr_right} (12 doubles)
+__device__ __forceinline__ void reconstruct(const Cons& ul, double zl, const Cons& ur, double zr,
+                                            double nx, double ny, const Phys& P, double* out) {
+  const double hls = zl >= zr ? ul.h : sel_max(0.0, ul.h + (zl - zr));
+  const double hrs = zr >= zl ? ur.h : sel_max(0.0, ur.h + (zr - zl));
+  Cons a = ul, b = ur;
+  if (!(hls == ul.h)) {
+    const double vx = ul.h < P.h_dry ? 0.0 : ul.qx / ul.h, vy = ul.h < P.h_dry ? 0.0 : ul.qy / ul.h;
+    a = Cons{hls, hls * vx, hls * vy};
+  }
+  if (!(hrs == ur.h)) {
+    const double vx = ur.h < P.h_dry ? 0.0 : ur.qx / ur.h, vy = ur.h < P.h_dry ? 0.0 : ur.qy / ur.h;
+    b = Cons{hrs, hrs * vx, hrs * vy};
+  }
+  const double pl = (0.5 * P.g) * ((ul.h * ul.h) - (hls * hls));
+  const double pr = (0.5 * P.g) * ((ur.h * ur.h) - (hrs * hrs));
+  const double v[12] = {a.h, a.qx, a.qy, b.h, b.qx, b.qy, 0.0, pl * nx, pl * ny, 0.0, pr * nx, pr * ny};
+  for (int k = 0; k < 12; ++k) out[k] = v[k];
+}
+
 // cell_signal_speed(), kernels.hpp:167-170 (called on wet cells only).
 __device__ __forceinline__ double signal_speed(const Cons& u, const Phys& P) {
   double vx, vy;

@@ -391,7 +391,103 @@ __global__ void k_point(int kind, long long n, Phys P, const double* l, const do
     out[3 * i + 2] = u.qy;
   } else if (kind == 4) {
     out[i] = swe_pow43(a.h);
+  } else if (kind == 5) {  // physical_flux_normal, kernels.hpp:21-27
+    const Flux f = normal_flux(a, nrm[2 * i], nrm[2 * i + 1], P);
+    out[3 * i] = f.m;
+    out[3 * i + 1] = f.fx;
+    out[3 * i + 2] = f.fy;
+  } else if (kind == 6) {  // wave_speed_estimates(l[0], l[1], r[0], r[1]), kernels.hpp:38-66
+    double SL, Ss, SR;
+    wave_speeds(a.h, a.qx, r[3 * i], r[3 * i + 1], P, SL, Ss, SR);
+    out[3 * i] = SL;
+    out[3 * i + 1] = Ss;
+    out[3 * i + 2] = SR;
+  } else if (kind == 7) {  // hydrostatic_reconstruct, kernels.hpp:126-152 -> out[12]
+    const Cons b{r[3 * i], r[3 * i + 1], r[3 * i + 2]};
+    reconstruct(a, z[2 * i], b, z[2 * i + 1], nrm[2 * i], nrm[2 * i + 1], P, out + 12 * i);
+  } else if (kind == 8) {  // cell_signal_speed, kernels.hpp:167-170
+    out[i] = signal_speed(a, P);
+  } else if (kind == 9) {  // clamp_dry, kernels.hpp:205-216 -> {h, qx, qy, clipped, throws}
+    const bool bad = a.h < -1e-14 * P.h_ref;
+    const bool neg = !bad && a.h < 0.0;
+    const bool dry = !bad && !neg && a.h < P.h_dry;
+    out[5 * i] = neg ? 0.0 : a.h;
+    out[5 * i + 1] = (neg || dry) ? 0.0 : a.qx;
+    out[5 * i + 2] = (neg || dry) ? 0.0 : a.qy;
+    out[5 * i + 3] = neg ? -a.h : 0.0;
+    out[5 * i + 4] = bad ? 1.0 : 0.0;
   }
+}
+
+// total_mass (engine.hpp:128-132) of host arrays: a fixed-order tree sum
+// (gridDim.x partials, each a fixed strided walk + shuffle tree; then one
+// block folds the partials), independent of the device it runs on
+__global__ void k_mass_parts(long long n, const double* h, const double* area, double* part) {
+  double m = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x)
+    m += h[i] * area[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  __shared__ double s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    part[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_mass_final(int n, const double* part, double* out) {
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m += part[i];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  __shared__ double s[32];
+  if ((threadIdx.x & 31) == 0) s[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += s[w];
+    *out = t;
+  }
+}
+
+// stable_dt (kernels.hpp:174-186) over arrays: the minimum of r / speed over
+// wet cells (an order-independent select-min, so the grid's order cannot
+// change it) and the lowest cell with a non-finite speed
+__device__ __forceinline__ void atomic_sel_min(double* p, double v) {
+  unsigned long long* a = reinterpret_cast<unsigned long long*>(p);
+  unsigned long long old = *a;
+  while (true) {
+    const double cur = __longlong_as_double((long long)old);
+    const double nv = sel_min(cur, v);
+    if (__double_as_longlong(nv) == __double_as_longlong(cur)) return;
+    const unsigned long long prev = atomicCAS(a, old, (unsigned long long)__double_as_longlong(nv));
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+__global__ void k_stable_dt(long long n, Phys P, const double* h, const double* qx,
+                            const double* qy, const double* inr, double* lo_out,
+                            unsigned long long* bad) {
+  double lo = INFINITY;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const Cons u{h[i], qx[i], qy[i]};
+    if (u.h < P.h_dry) continue;
+    const double s = signal_speed(u, P);
+    if (!isfinite(s)) {
+      atomicMin(bad, (unsigned long long)i);
+      continue;
+    }
+    lo = sel_min(lo, inr[i] / s);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lo = sel_min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+  if ((threadIdx.x & 31) == 0 && lo < INFINITY) atomic_sel_min(lo_out, lo);
 }
 
 }  // namespace swe_b200

@@ -94,6 +94,57 @@ int main() {
                 }());
   }
 
+  {  // the device cache follows the Mesh's CONTENT: a bed mutated in place and a
+     // new Mesh on recycled addresses are re-uploaded; helpers
+     // called from on_snapshot during run() do not disturb the run
+    CaseSpec spec = make_case(CaseId::three_mounds);
+    const RawMesh raw = generate_square_mesh(40, 16, spec.lx, spec.ly);
+    CaseSetup setup = setup_case(spec, raw);
+    auto steps = [&](const Mesh& m, int n) {
+      Simulation sim;
+      sim.current = setup.state;
+      sim.next.resize(m.n_cells());
+      EdgeFluxes f;
+      for (int k = 0; k < n; ++k) advance_step(sim, m, params, {}, 1e9, f);
+      return sim.current.h;
+    };
+    Mesh m = setup.mesh;
+    const std::vector<double> h0 = steps(m, 20);
+    for (double& z : m.cell_bed) z *= 0.5;  // in place: same addresses and sizes
+    const std::vector<double> h1 = steps(m, 20);
+    const Mesh fresh = m;  // a distinct Mesh with the mutated bed
+    const std::vector<double> h2 = steps(fresh, 20);
+    const bool mutation_ok = h1 == h2 && h1 != h0;
+
+    Simulation a;
+    a.current = setup.state;
+    a.next.resize(m.n_cells());
+    Simulation b = a;
+    RunOptions opt;
+    opt.t_end = 3.0;
+    opt.snapshot_interval = 0.5;
+    int calls = 0;
+    double mass_in_cb = 0.0;
+    opt.on_snapshot = [&](const FieldState& s, double, long) {
+      ++calls;
+      mass_in_cb = total_mass(s, m);  // reference-legal inside a run
+      EdgeFluxes f;
+      compute_fluxes(s, m, params, {}, f);
+      Simulation other;
+      other.current = s;
+      other.next.resize(m.n_cells());
+      advance_step(other, m, params, {}, 1e9, f);
+    };
+    const RunStats ra = run(a, m, params, {}, opt);
+    opt.on_snapshot = nullptr;
+    const RunStats rb = run(b, m, params, {}, opt);
+    const bool reentrant_ok = calls > 3 && ra.steps == rb.steps && ra.t_final == rb.t_final &&
+                              a.current.h == b.current.h && a.current.qx == b.current.qx &&
+                              mass_in_cb > 0.0;
+    std::printf("\"cache_mutation_ok\": %s, \"reentrant_ok\": %s, ", mutation_ok ? "true" : "false",
+                reentrant_ok ? "true" : "false");
+  }
+
   {  // errors keep the reference's types and messages (test_engine.cpp:218-247)
     const RawMesh raw = generate_square_mesh(3, 3, 1.0, 1.0);
     const Mesh m = build_mesh(raw, std::vector<double>(18, 0.0), std::vector<double>(18, 0.0));

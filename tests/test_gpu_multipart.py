@@ -107,6 +107,28 @@ def test_linked_single_rank_graph_matches_unlinked():
     assert bit_equal(recs[:, 2], ref[:, 2]) and bit_equal(recs[:, 3], ref[:, 3])
 
 
+def test_link_normalises_buffer_parity_after_unlinked_steps():
+    """A part stepped an odd number of times before linking (its state in
+    buffer 1) still exchanges correctly: swe_dev_link moves every rank's
+    current state to buffer 0 (pushes target the sender's cur^1)."""
+    sc, m, lms = _scenario_parts(2)
+    parts = [dist.LinkedPart(lm) for lm in lms]
+    parts[0].set_state(sc.state)
+    parts[0].advance(max_steps=1)  # unlinked warm-up: part 0 now holds cur = 1
+    dist.link_local(parts)
+    for p in parts:
+        p.set_state(sc.state)
+    recs = dist.run_lockstep(parts, 40)
+    got = api.FieldState.zeros(m.n_cells)
+    for p in parts:
+        p.gather_owned(got)
+    ref = COracle().advance(MeshArrays.from_mesh(m), sc.state.h, sc.state.qx, sc.state.qy,
+                            nsteps=40)
+    assert bit_equal(recs[:, 2], ref["dts"])
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(got, k), ref[k]), k
+
+
 def test_linked_error_reports_global_index():
     sc, m, lms = _scenario_parts(2)
     parts = [dist.LinkedPart(lm) for lm in lms]

@@ -351,6 +351,8 @@ def test_cpp_drop_in_driver(golden):
     assert out["nan_msg"] == "stable_dt: non-finite velocity in cell 5"
     assert out["neg_msg"].startswith("compute_fluxes: negative depth at edge ")
     assert out["cfg_msg"] == "run: t_end must be > 0"
+    # the device cache keys on content; helpers inside on_snapshot leave run() intact
+    assert out["cache_mutation_ok"] and out["reentrant_ok"]
 
 
 def test_advance_async_equals_advance():
