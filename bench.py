@@ -164,43 +164,86 @@ def build_workload(name, scale, device=None):
     return sc, mesh, time.perf_counter() - t0
 
 
-def workload_config(name, sc, mesh, world, note_extra=None):
-    cfg = {"workload": f"{name} ({CONFIG_NOTE[name]})", "cells": mesh.n_cells,
-           "edges": mesh.n_edges, "boundary_edges": mesh.n_boundary_edges,
-           "mesh": "unstructured: jittered nodes, random diagonals, random node/cell numbering",
-           "l2": ("inputs larger than L2 (state + mesh ~= 300 B/cell >> 126 MB)"
-                  if 300 * mesh.n_cells > 2 * 126e6 else
-                  f"inputs fit in L2 (~{300 * mesh.n_cells / 1e6:.0f} MB of state + mesh): "
-                  "resident across steps as in any run of this size; not flushed"),
-           "parallelism": "single GPU" if world == 1 else f"{world} independent replicas"}
-    if note_extra:
-        cfg.update(note_extra)
-    return cfg
+def produce_workload(name, scale):
+    """The same inputs from a producer SUBPROCESS (tools/make_workload.py), so
+    the process that runs the reference never loads libswe_b200.so."""
+    import tempfile
+    with tempfile.TemporaryDirectory(prefix="swe_wl_") as d:
+        out = Path(d) / "w.npz"
+        subprocess.run([sys.executable, str(ROOT / "tools" / "make_workload.py"), "--config", name,
+                        "--scale", repr(scale), "--out", str(out)], check=True)
+        with np.load(out) as z:
+            return {k: z[k] for k in z.files}
+
+
+def workload_config(name, n_cells, n_edges, n_boundary, world):
+    """identical in both arms (the driver compares the two lines' config)"""
+    return {"workload": f"{name} ({CONFIG_NOTE[name]})", "cells": n_cells,
+            "edges": n_edges, "boundary_edges": n_boundary,
+            "mesh": "unstructured: jittered nodes, random diagonals, random node/cell numbering",
+            "l2": ("inputs larger than L2 (state + mesh ~= 300 B/cell >> 126 MB)"
+                   if 300 * n_cells > 2 * 126e6 else
+                   f"inputs fit in L2 (~{300 * n_cells / 1e6:.0f} MB of state + mesh): "
+                   "resident across steps as in any run of this size; not flushed"),
+            "step_window": "steps [W, W+K) from the initial state (W = --warmup, at least 3) in "
+                           "both arms",
+            "parallelism": "single GPU" if world == 1 else f"{world} GPUs"}
 
 
 REF_MAX_STEPS = 150
+HORIZON = 1.7976931348623157e308  # bench.hpp:91 (fixed-step throughput mode)
 
 
 def reference_threads():
     return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 
 
-def time_reference(sc, mesh, steps, warmup, threads):
-    """The reference (oracle/_ref, unmodified headers) on the same mesh and
-    initial state; phase timers of engine.hpp:314-317 as bench.hpp:105-110."""
-    from oracle.pyoracle import RefOracle
-    ref = RefOracle()
-    t0 = time.perf_counter()
-    rm = ref.build_mesh(sc.raw.nodes, sc.raw.triangles, sc.bed, sc.manning)
-    setup_s = time.perf_counter() - t0
-    st = sc.state
-    if warmup > 0:
-        rm.advance(st.h, st.qx, st.qy, t_end=1.7976931348623157e308, nsteps=warmup, threads=threads)
-    r = rm.advance(st.h, st.qx, st.qy, t_end=1.7976931348623157e308, nsteps=steps, threads=threads)
+def host_cpu_info():
+    """core counts of the host (state the count)"""
+    info = {"hardware_concurrency": os.cpu_count(), "affinity_threads": reference_threads()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {k.strip(): v.strip() for k, v in
+              (ln.split(":", 1) for ln in out.splitlines() if ":" in ln)}
+        info["lscpu_cpus"] = int(kv.get("CPU(s)", 0) or 0)
+        cps, sk = int(kv.get("Core(s) per socket", 0) or 0), int(kv.get("Socket(s)", 0) or 0)
+        info["lscpu_physical_cores"] = cps * sk if cps and sk else None
+        info["lscpu_threads_per_core"] = int(kv.get("Thread(s) per core", 0) or 0) or None
+        info["model"] = kv.get("Model name")
+    except Exception as e:  # lscpu missing: hardware_concurrency only
+        info["lscpu"] = f"unavailable ({type(e).__name__})"
+    return info
+
+
+def reference_window(rm, st, W, K, threads, seq_steps=0):
+    """The reference (oracle/_ref, unmodified headers) from the initial state:
+    W untimed steps on all threads, then K steps timed by its own phase
+    timers (engine.hpp:314-317, as bench.hpp:105-110) with `threads`; with
+    seq_steps, also that many steps of the same window on ONE thread."""
+    r0 = rm.advance(st["h"], st["qx"], st["qy"], t_end=HORIZON, nsteps=W, threads=threads)
+    if r0["rc"] != 0:
+        raise RuntimeError(f"reference failed: {r0['error']}")
+    at = dict(t=r0["t"], step=r0["step"], clipped_volume=r0["clipped_volume"],
+              clip_events=r0["clip_events"])
+    r = rm.advance(r0["h"], r0["qx"], r0["qy"], t_end=HORIZON, nsteps=K, threads=threads, **at)
     if r["rc"] != 0:
         raise RuntimeError(f"reference failed: {r['error']}")
     phase_s = r["flux_s"] + r["update_s"]
-    return mesh.n_cells * steps / phase_s, phase_s, setup_s
+    out = {"value": rm.n_cells * K / phase_s, "phase_s": phase_s, "steps": K,
+           "state": (r["h"], r["qx"], r["qy"]), "dts": r["dts"]}
+    if seq_steps:
+        q = rm.advance(r0["h"], r0["qx"], r0["qy"], t_end=HORIZON, nsteps=seq_steps, threads=1, **at)
+        out["seq_value"] = rm.n_cells * seq_steps / (q["flux_s"] + q["update_s"])
+        out["seq_steps"] = seq_steps
+    return out
+
+
+def ref_mesh_of(wl):
+    from oracle.pyoracle import RefOracle
+    ref = RefOracle()
+    t0 = time.perf_counter()
+    rm = ref.build_mesh(wl["nodes"], wl["tris"], wl["bed"], wl["manning"])
+    return rm, time.perf_counter() - t0
 
 
 def run_reference(args):
@@ -212,24 +255,44 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libswe_ref.so was not built (needs /root/reference)"}))
         return
-    sc, mesh, _ = build_workload(args.config, args.scale)
+    scale = args.scale * (world ** 0.5 if args.scaling == "weak" and world > 1 else 1.0)
+    wl = produce_workload(args.config, scale)
+    rm, build_s = ref_mesh_of(wl)
     threads = reference_threads()
     # bounded sample: ~0.34 s per step at 10M cells on 16 threads, so at most
     # REF_MAX_STEPS timed steps keep the arm within a few minutes for any K
-    steps, warmup = min(args.steps, REF_MAX_STEPS), min(args.warmup, 3)
-    value, phase_s, setup_s = time_reference(sc, mesh, steps, warmup, threads)
-    sample = (f"{steps} timed steps (after {warmup} warm-up) of the full "
-              f"{mesh.n_cells}-cell workload, reference build with -O3 -fopenmp "
-              f"-ffp-contract=off, {threads} OpenMP threads, phase timers")
-    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": 1e3 * phase_s / steps, "higher_is_better": True,
+    W, K = max(3, args.warmup), min(args.steps, REF_MAX_STEPS)
+    r = reference_window(rm, wl, W, K, threads)
+    sample = (f"steps [{W}, {W + K}) of the full {rm.n_cells}-cell workload (the B200 arm's window"
+              f"{'' if K == args.steps else ', first ' + str(K) + ' of its ' + str(args.steps) + ' steps'}"
+              f"), reference built with -O3 -fopenmp -ffp-contract=off, {threads} OpenMP threads, "
+              "its own phase timers; inputs from a producer subprocess, mesh from the reference's "
+              "build_mesh")
+    out = {"impl": "reference", "metric": METRIC, "value": r["value"], "unit": UNIT,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * r["phase_s"] / K, "higher_is_better": True,
            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_config(args.config, sc, mesh, 1),
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-                            "sample": sample},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+           "config": workload_config(args.config, rm.n_cells, rm.n_edges, rm.n_boundary,
+                                     args.gpus),
+           "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads,
+                            "kind": "reference", "sample": sample, "host": host_cpu_info()},
+           "e2e": {"value": r["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0},
+           "setup": {"reference_build_mesh_s": round(build_s, 2)},
+           "native_libs": repo_libs_mapped()}
     print(json.dumps(out))
+
+
+def repo_libs_mapped():
+    """shared objects of this repo mapped into this process (/proc/self/maps):
+    the reference arm's must be oracle/ libraries only"""
+    try:
+        maps = Path("/proc/self/maps").read_text().splitlines()
+    except OSError:
+        return None
+    root = str(ROOT.resolve())
+    libs = {ln.split()[-1] for ln in maps if ln.rstrip().endswith(".so") and root in ln}
+    return sorted(str(Path(x).resolve().relative_to(ROOT.resolve())) for x in libs)
 
 
 def run_b200_dist(args, rank, local, world):
@@ -259,7 +322,7 @@ def run_b200_dist(args, rank, local, world):
         return run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s,
                                     reason=str(e))
     lp.set_state(sc.state)
-    horizon = 1.7976931348623157e308
+    horizon = HORIZON
     W, K = max(3, args.warmup), args.steps
     dev = "cpu" if LOCKSTEP_CHECK else "cuda"
 
@@ -277,17 +340,21 @@ def run_b200_dist(args, rank, local, world):
     def records():
         return launch.recs if LOCKSTEP_CHECK else lp.records()
 
-    advance(W)
-    # clocks ramp: keep stepping >= 1 s; every rank takes the same decision
+    # clocks ramp: keep stepping >= 1 s (every rank takes the same decision),
+    # then restart from the initial state: the timed window is steps [W, W+K),
+    # the reference arm's
     t_w = time.perf_counter()
-    steps = W
-    while True:
+    steps = 0
+    while not LOCKSTEP_CHECK:
         go = torch.tensor([1.0 if time.perf_counter() - t_w < 1.0 else 0.0], device=dev)
         tdist.all_reduce(go, op=tdist.ReduceOp.MAX)
         if go.item() == 0.0:
             break
         steps += 50
         advance(steps)
+    lp.set_state(sc.state)
+    advance(W)
+    steps = W
     skipped0 = lp_skipped(lp)
     stream = torch.cuda.ExternalStream(dist_stream(lp), device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -312,11 +379,21 @@ def run_b200_dist(args, rank, local, world):
     skip_frac = float(sk[0].item()) / max(1.0, float(sk[1].item()))
     ms = float(ms.item())
     C = mesh.n_cells
-    # e2e: host state in, K steps, owned state back to the host
+    # e2e: host state in, the same K steps, owned state back to the host
+    # (the state at step W -- the window's start -- is re-formed untimed)
+    lp.set_state(sc.state)
+    advance(W)
+    start = api.FieldState.zeros(mesh.n_cells)
+    t_start, _ = lp.gather_owned(start)
+    gath = [None] * world
+    tdist.all_gather_object(gath, (lm.cells[:lm.n_owned], start.h[lm.cells[:lm.n_owned]],
+                                   start.qx[lm.cells[:lm.n_owned]], start.qy[lm.cells[:lm.n_owned]]))
+    for cells, h, qx, qy in gath:
+        start.h[cells], start.qx[cells], start.qy[cells] = h, qx, qy
     tdist.barrier()
     t0 = time.perf_counter()
-    lp.set_state(sc.state)
-    advance(K)
+    lp.set_state(start, t=t_start, step=W)
+    advance(W + K)
     got = api.FieldState.zeros(C)
     lp.gather_owned(got)
     e2e_s = torch.tensor([time.perf_counter() - t0], device=dev)
@@ -325,18 +402,21 @@ def run_b200_dist(args, rank, local, world):
         out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": workload_config(args.config, sc, mesh, 1, {
-                   "parallelism": f"{world}-way cost-weighted RCB domain decomposition (cells "
-                                  "of computed tiles weighted "
-                                  f"{dist.COMPUTED_COST_LARGE if mesh.n_cells / world >= dist.LARGE_PART_CELLS else dist.COMPUTED_COST}"
-                                  "x cells of skipped dry tiles, measured on the device), one "
-                                  "part per GPU; "
-                                  "ghost states pushed peer-to-peer by the step kernel, CFL "
-                                  "bound / outcome through device mailboxes (no host round "
-                                  "trip per step)",
+               "config": workload_config(args.config, mesh.n_cells, mesh.n_edges,
+                                         mesh.n_boundary_edges, world),
+               "decomposition": {
+                   "how": f"{world}-way cost-weighted RCB domain decomposition (cells "
+                          "of computed tiles weighted "
+                          f"{dist.COMPUTED_COST_LARGE if mesh.n_cells / world >= dist.LARGE_PART_CELLS else dist.COMPUTED_COST}"
+                          "x cells of skipped dry tiles, measured on the device), one "
+                          "part per GPU; "
+                          "ghost states pushed peer-to-peer by the step kernel, CFL "
+                          "bound / outcome through device mailboxes (no host round "
+                          "trip per step)",
                    "cells_per_gpu_max": int(np.bincount(part).max()),
                    "cells_per_gpu_min": int(np.bincount(part).min()),
-                   "halo_cells_rank0": int(lm.n_cells - lm.n_owned), "setup_s": round(setup_s, 2)}),
+                   "halo_cells_rank0": int(lm.n_cells - lm.n_owned)},
+               "setup": {"setup_s": round(setup_s, 2)},
                "gpu_launches": 2 * U * -(-K // U) + 2,
                "gpu_launches_note": "per rank: k_set_params + one CUDA-graph launch = k_gate + "
                                     f"a conditional WHILE node of ceil(K/{U}) iterations x {U} x "
@@ -403,12 +483,14 @@ def run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s, 
         out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": workload_config(args.config, sc, mesh, 1, {
-                   "parallelism": f"{world}-way cost-weighted RCB domain decomposition, host-"
-                                  "driven exchange (NCCL send/recv + all_reduce per step): "
-                                  f"linked peer memory unavailable ({reason[:160]})",
-                   "cells_per_gpu_max": int(np.bincount(part).max()),
-                   "setup_s": round(setup_s, 2)}),
+               "config": workload_config(args.config, mesh.n_cells, mesh.n_edges,
+                                         mesh.n_boundary_edges, world),
+               "decomposition": {
+                   "how": f"{world}-way cost-weighted RCB domain decomposition, host-"
+                          "driven exchange (NCCL send/recv + all_reduce per step): "
+                          f"linked peer memory unavailable ({reason[:160]})",
+                   "cells_per_gpu_max": int(np.bincount(part).max())},
+               "setup": {"setup_s": round(setup_s, 2)},
                "gpu_launches": launches,
                "gpu_launches_note": "rank 0, counted by the library: per step halo pack / "
                                     "unpack, k_set_params, k_gate, k_tile, k_finalize (+ NCCL "
@@ -483,17 +565,21 @@ def run_b200(args):
     t0 = time.perf_counter()
     solver = api.DeviceSolver(mesh, device=local)
     create_s = time.perf_counter() - t0
-    solver.set_state(sc.state)
-    horizon = 1.7976931348623157e308  # bench.hpp:91 (fixed-step throughput mode)
+    horizon = HORIZON
     W, K = max(3, args.warmup), args.steps
     clk = ClockSampler(local).start()
-    solver.advance(t_end=horizon, max_steps=W)
-    # clocks ramp from idle: keep stepping (untimed) for >= 1 s before timing
+    # clocks ramp from idle: >= 1 s of untimed stepping, then restart from the
+    # initial state so the timed window is steps [W, W+K) -- the reference
+    # arm's window (the W warm-up steps also rebuild the dry-tile mask)
+    solver.set_state(sc.state)
     t_w = time.perf_counter()
     while time.perf_counter() - t_w < 1.0:
         _, s_now = solver.clock()
         solver.advance(t_end=horizon, max_steps=s_now + 50)
+    solver.set_state(sc.state)
+    solver.advance(t_end=horizon, max_steps=W)
     _, step0 = solver.clock()
+    assert step0 == W
     skipped0 = solver.info()["skipped_tiles"]
     # e2e replays the same K steps from this state (untimed copy-out here)
     e2e_start = None if args.no_e2e else solver.get_state()
@@ -524,8 +610,11 @@ def run_b200(args):
         dist.barrier()
     value = world * C * K / (ms / 1e3)
 
-    # kernel-level timing: same K steps, plain launches with events per kernel
-    skipped1 = info0["skipped_tiles"]
+    # kernel-level timing: the same K steps again (from the state at step W),
+    # plain launches with events per kernel on the solver's stream
+    solver.set_state(sc.state)
+    solver.advance(t_end=horizon, max_steps=W)
+    skipped1 = solver.info()["skipped_tiles"]
     solver.set_profiling(True)
     solver.advance_n_async(K, t_end=horizon)
     solver.synchronize()
@@ -536,42 +625,59 @@ def run_b200(args):
     avg = lambda k: kt[k][0] / max(1, kt[k][1])  # noqa: E731
     fin_ms = avg("finalize")
     peak, peak_src = load_peaks()
+    step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical B_step
+    step_eff = (1.0 - skip_frac) * step_bytes + skip_frac * 40 * C  # skipped tiles: 40 B/cell
+    prof = load_traffic()
     if info["fused"]:
-        # k_tile compulsory traffic: cell state/bed/area/n/r in (56 B) + state
-        # out (24 B); edge record {el|kl, er|kr} (8 B) + {nx, ny} (16 B) + len
-        # (8 B) = 32 B; halo index (4 B)
-        # a dry tile skipped moves 40 B per cell: h and area in,
-        # state out -- no edge data, no qx / qy / bed
+        # the dominant kernel k_tile does the whole step (face + cell work of
+        # §8(d)) in one launch: its algorithmic bytes per launch are B_step,
+        # skipped dry tiles counted at 40 B/cell (h, area in; state out)
         tile_ms = avg("tile")
         kernels = {"tile": tile_ms, "finalize": fin_ms}
-        full = 80 * C + 32 * E + 4 * info["halo_edges"]
-        dom = ("tile", tile_ms, (1.0 - prof_skip) * full + prof_skip * 40 * C)
+        own = 80 * C + 32 * E + 4 * info["halo_edges"]  # the fused kernel's own compulsory bytes
+        dom = ("tile", tile_ms, (1.0 - prof_skip) * step_bytes + prof_skip * 40 * C,
+               (1.0 - prof_skip) * own + prof_skip * 40 * C)
     else:
-        # k_face_c: edge data 34 B + contributions out 48 B per edge, state+bed
-        # gathers 32 B per cell; k_cell_c: 3x3 contributions 72 B + state 24 B
-        # + area/n/r 24 B in, state 24 B out per cell
         face_ms, cell_ms = avg("face"), avg("cell")
         kernels = {"face": face_ms, "cell": cell_ms, "finalize": fin_ms}
-        dom = (("face", face_ms, 82 * E + 32 * C) if face_ms >= cell_ms
-               else ("cell", cell_ms, 144 * C))
-    achieved = dom[2] / (dom[1] / 1e3) / 1e9
-    step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical two-phase B_step
-    step_eff = (1.0 - skip_frac) * step_bytes + skip_frac * 40 * C  # skipped tiles: 40 B/cell
-    traffic, limiter = None, None
-    prof = ROOT / "profiles" / "traffic.json"
-    if prof.exists():
-        try:
-            tj = json.loads(prof.read_text())
-            traffic, limiter = tj.get(dom[0]), tj.get(dom[0] + "_limiter")
-        except Exception:
-            traffic = None
+        dom = (("face", face_ms, 64 * E + 32 * C, 82 * E + 32 * C) if face_ms >= cell_ms
+               else ("cell", cell_ms, 64 * E + 84 * C, 144 * C))
+    t_s = dom[1] / 1e3
+    achieved = dom[2] / t_s / 1e9
+    traffic = prof.get(dom[0])
+    fp64 = prof.get(dom[0] + "_fp64_thread_inst")
+    fpk = load_fp64_peak()
+    roof = {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
+            "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+            "peak_source": peak_src,
+            "canonical_frac": achieved / peak,
+            "canonical_bytes_per_launch": dom[2],
+            "canonical_note": "SURVEY.md 8(d) B_step = 116 C + 128 E per step (one k_tile "
+                              "launch), dry tiles skipped in this window counted at 40 B/cell",
+            "dram_frac": (traffic / t_s / 1e9 / peak) if traffic else None,
+            "dram_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch "
+                         "(committed capture, profiles/traffic.json) over this run's mean launch "
+                         "time: the physical HBM utilisation",
+            "fp64_frac": (fp64 / t_s / fpk["dfma_per_s"]) if (fp64 and fpk) else None,
+            "fp64_note": ("FP64 thread-instructions (DFMA + DMUL + DADD) per launch from the ncu "
+                          "capture over the mean launch time, against the measured DFMA peak "
+                          f"{fpk['dfma_per_s']:.3e}/s (profiles/r02_fp64_peak.json)") if fpk else
+                         "no FP64 peak measured",
+            "own_bytes_per_launch": dom[3],
+            "own_frac": dom[3] / t_s / 1e9 / peak,
+            "limiter": prof.get(dom[0] + "_limiter"),
+            "kernel_ms": kernels,
+            "layout": info,
+            "step": {"algorithmic_bytes": step_eff,
+                     "achieved_gbs": step_eff / (ms / K / 1e3) / 1e9,
+                     "frac": step_eff / (ms / K / 1e3) / 1e9 / peak}}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K,
            "warmup": W, "ms_per_step": ms / K, "higher_is_better": True, "scaling": args.scaling,
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_config(args.config, sc, mesh, world,
-                                     {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
-                                      "device_bytes": solver.memory_bytes()}),
+           "config": workload_config(args.config, C, E, mesh.n_boundary_edges, world),
+           "setup": {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
+                     "device_bytes": solver.memory_bytes()},
            "gpu_launches": (2 if info["fused"] else 3) * info["graph_unroll"]
                            * -(-K // info["graph_unroll"]) + 2,
            "gpu_launches_note": "k_set_params + one CUDA-graph launch = k_gate + a conditional "
@@ -580,18 +686,7 @@ def run_b200(args):
                                 + ("k_tile" if info["fused"] else "k_face_c, k_cell_c")
                                 + ", k_finalize); steps past the stop exit at once "
                                 f"(host-side launch calls: {launches})",
-           "roofline": {"bound": "hbm", "kernel": dom[0], "achieved": achieved, "peak": peak,
-                        "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                        "peak_source": peak_src,
-                        "limiter": limiter,
-                        "algorithmic_bytes_per_launch": dom[2],
-                        "kernel_ms": kernels,
-                        "layout": info,
-                        "step": {"canonical_bytes": "SURVEY.md 8(d) B_step = 116 C + 128 E, "
-                                                    "skipped dry tiles counted at 40 B/cell",
-                                 "algorithmic_bytes": step_eff,
-                                 "achieved_gbs": step_eff / (ms / K / 1e3) / 1e9,
-                                 "frac": step_eff / (ms / K / 1e3) / 1e9 / peak}},
+           "roofline": roof,
            "clocks": clk.summary()}
     if info["fused"]:
         ms_ns = (no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch)
@@ -607,11 +702,27 @@ def run_b200(args):
     if not args.no_e2e:
         out["e2e"] = e2e_run(api, solver, e2e_start, K, horizon, torch)
     if rank == 0 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(sc, mesh, args)
+        out["cpu_baseline"] = cpu_baseline(sc, mesh, args, W)
     if rank == 0:
         print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "traffic.json"
+    try:
+        return json.loads(p.read_text()) if p.exists() else {}
+    except Exception:
+        return {}
+
+
+def load_fp64_peak():
+    p = ROOT / "profiles" / "r02_fp64_peak.json"
+    try:
+        return json.loads(p.read_text()) if p.exists() else None
+    except Exception:
+        return None
 
 
 def no_skip_ms(api, mesh, sc, step0, K, horizon, local, torch):
@@ -665,20 +776,30 @@ def e2e_run(api, solver, start, K, horizon, torch):
                     "(from the state at its first timed step)"}
 
 
-def cpu_baseline(sc, mesh, args):
+def cpu_baseline(sc, mesh, args, W):
+    """The reference (oracle/_ref) on a bounded sample of the same window:
+    steps [W, W+k) on all host threads, and a few of them on one thread
+    (bench.hpp:150-153 times a sequential and a parallel variant)."""
     from oracle.pyoracle import RefOracle
     if not RefOracle.available():
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                 "sample": "unavailable: oracle/_ref not built"}
     threads = reference_threads()
-    # size the sample to ~cpu_seconds of work at ~5e7 cell-updates/s/8 threads
-    est = 6e6 * threads
-    steps = int(max(2, min(50, args.cpu_seconds * est / mesh.n_cells)))
-    value, phase_s, setup_s = time_reference(sc, mesh, steps, 1, threads)
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "reference",
-            "sample": f"{steps} steps of the full {mesh.n_cells}-cell workload after 1 warm-up "
-                      f"step ({phase_s:.1f} s of phase time, reference build_mesh {setup_s:.1f} s "
-                      f"excluded), {threads} OpenMP threads"}
+    wl = {"nodes": sc.raw.nodes, "tris": sc.raw.triangles, "bed": sc.bed, "manning": sc.manning,
+          "h": sc.state.h, "qx": sc.state.qx, "qy": sc.state.qy}
+    rm, build_s = ref_mesh_of(wl)
+    # size the samples to ~cpu_seconds of work (~5e7 cell-updates/s on 8 threads,
+    # ~8e6 on one)
+    steps = int(max(2, min(args.steps, 50, args.cpu_seconds * 6e6 * threads / mesh.n_cells)))
+    seq = int(max(1, min(steps, 0.5 * args.cpu_seconds * 8e6 / mesh.n_cells)))
+    r = reference_window(rm, wl, W, steps, threads, seq_steps=seq)
+    return {"value": r["value"], "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"steps [{W}, {W + steps}) of the full {mesh.n_cells}-cell workload "
+                      f"({r['phase_s']:.1f} s of phase time, reference build_mesh {build_s:.1f} s "
+                      f"excluded), {threads} OpenMP threads",
+            "sequential": {"value": r["seq_value"], "unit": UNIT, "cores": 1,
+                           "sample": f"steps [{W}, {W + seq}) on one thread"},
+            "host": host_cpu_info()}
 
 
 def main():

@@ -49,4 +49,21 @@ def test_reference_arm_bounds_its_sample():
     d = run_bench("--impl", "reference", "--config", "circular_dam_break", "--steps",
                   str(bench.REF_MAX_STEPS + 5), "--warmup", "1")
     assert d["steps"] == bench.REF_MAX_STEPS + 5
-    assert f"{bench.REF_MAX_STEPS} timed steps" in d["cpu_baseline"]["sample"]
+    assert f"first {bench.REF_MAX_STEPS} of its {bench.REF_MAX_STEPS + 5} steps" in \
+        d["cpu_baseline"]["sample"]
+
+
+def test_reference_arm_runs_the_reference_only():
+    """The reference process maps no library of this repo except oracle/'s
+    (inputs come from a producer subprocess), and its config equals the B200
+    arm's workload_config on the same mesh (same step window)."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    d = run_bench("--impl", "reference", "--config", "circular_dam_break", "--steps", "3",
+                  "--warmup", "2")
+    libs = d["native_libs"]
+    assert libs and all(x.startswith("oracle/") for x in libs), libs
+    assert d["config"] == bench.workload_config("circular_dam_break", 10082, d["config"]["edges"],
+                                                d["config"]["boundary_edges"], 1)
+    assert d["cpu_baseline"]["host"]["hardware_concurrency"] >= 1
+    assert "steps [3, 6)" in d["cpu_baseline"]["sample"]

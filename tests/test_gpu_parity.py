@@ -517,24 +517,26 @@ def test_dry_skip_long_runs_equal_no_skip(monkeypatch, config, scale, steps):
 
 @pytest.mark.parametrize("config", ["channel", "sloping_wet_dry"])
 def test_full_size_steps_bitwise_vs_reference(refo, config):
-    """BASELINE configs [2] / [3] at FULL size (10.26M cells): 12 device steps
-    (dry-tile skipping on, Morton tiles) equal the reference's own
-    advance_step (oracle/_ref, all host threads) bit for bit -- state, dt,
-    max speed and the clip ledger's event count."""
+    """BASELINE configs [2] / [3] at FULL size (10.26M cells): the bench's
+    timed window -- steps [W, W+K) = [5, 25) from the initial state with the
+    driver's --warmup 5 --steps 20 -- on the device (dry-tile skipping on)
+    equals the reference's own advance_step (oracle/_ref, all host threads)
+    bit for bit: state, dt, max speed and the clip ledger's event count."""
     import os
+    n = 25
     sc = api.make_scenario(config)
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
     s = api.DeviceSolver(mesh)
     s.set_state(sc.state)
-    recs = s.advance(1e30, max_steps=12)
+    recs = s.advance(1e30, max_steps=n)
     got, _, _ = s.get_state()
     _, ev = s.ledger()
     info = s.info()
     s.close()
     rm = refo.build_mesh(sc.raw.nodes, sc.raw.triangles, sc.bed, sc.manning)
-    r = rm.advance(sc.state.h, sc.state.qx, sc.state.qy, t_end=1e30, nsteps=12,
+    r = rm.advance(sc.state.h, sc.state.qx, sc.state.qy, t_end=1e30, nsteps=n,
                    threads=len(os.sched_getaffinity(0)))
-    assert r["rc"] == 0 and r["done"] == 12
+    assert r["rc"] == 0 and r["done"] == n
     assert info["dry_skip"] == 1 and info["skipped_tiles"] > 0
     assert bit_equal(recs[:, 2], r["dts"]) and bit_equal(recs[:, 3], r["max_speeds"])
     assert ev == r["clip_events"]
