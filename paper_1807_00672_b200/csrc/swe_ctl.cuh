@@ -20,6 +20,7 @@ struct StepParams {  // written by the host before a launch sequence
   long long rec_cap;
   int ring;  // records wrap instead of stopping the loop
   int mode;  // 0 run loop, 1 single advance_step (no t/max_steps gate), 2 flux only
+  long long add_steps;  // > 0: the gate sets max_steps = step + add_steps (exactly n steps)
 };
 
 struct Ctl {
@@ -106,6 +107,16 @@ struct Link {
   unsigned long long timeout_ns;
 };
 
+// Step barrier of the persistent step kernel (k_run): CTAs count their
+// arrivals at the end of every step (monotonic within a launch); the last to
+// arrive commits the step and publishes it as the next epoch.  k_gate resets
+// both before a launch.  One 128-byte line.
+struct __align__(128) Sync {
+  unsigned int arrive;
+  unsigned int epoch;
+  unsigned int pad[30];
+};
+
 struct __align__(32) CellGeo {
   double z, area, man, inr;
 };
@@ -151,6 +162,13 @@ struct Dev {
   int* skipmask;
   const int *nbr_off, *nbr;
   const int* soff;
+  // persistent step kernel (k_run): barrier, double-buffered dry-tile flags
+  // pflag[(step & 1) * ntiles + t] = tag of the state `step` if tile t is dry
+  // and at rest in it (written during the previous step, read in this one),
+  // tiles with an edge on a ghost cell (linked: they wait for the exchange)
+  Sync* sync;
+  int* pflag;
+  const unsigned char* tile_ghost;
   const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
   const double *snx, *sny, *slen;
   // state, double-buffered
@@ -176,6 +194,16 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
 
 __device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
 __device__ __forceinline__ unsigned long long global_ns() {
@@ -324,9 +352,17 @@ __global__ void k_set_params(StepParams* sp, StepParams v) { *sp = v; }
 // gate: opens a launch sequence (run() loop entry, engine.hpp:355-358)
 __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   Ctl* c = d.ctl;
-  const StepParams* sp = d.sp;
+  StepParams* sp = const_cast<StepParams*>(d.sp);
+  if (sp->add_steps > 0) {
+    sp->max_steps = c->step + sp->add_steps;
+    sp->add_steps = 0;
+  }
   c->status = SWE_OK;
   c->n_rec = 0;
+  if (d.sync) {  // the persistent kernel's barrier starts over with every launch
+    d.sync->arrive = 0;
+    d.sync->epoch = 0;
+  }
   c->tile_next = 0;
   c->bad_edge = kNone;
   c->bad_cell = kNone;

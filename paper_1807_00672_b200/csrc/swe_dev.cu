@@ -94,6 +94,8 @@ struct swe_dev_ctx {
   bool cfl_posted = false;  // link_phase: a CFL exchange awaits its wait
   bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
   int graph_unroll = 8;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
+  bool persistent = false;      // run loop = one cooperative k_run launch (SWE_PERSISTENT=0: graph)
+  int grid_run = 0;             // CTAs of k_run (= grid_tile when the occupancies agree)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
   // asynchronous snapshots: device staging slots, copy stream, events
@@ -207,6 +209,21 @@ int launch_gate(swe_dev_ctx* x) {
   return cuda_ok(cudaGetLastError(), "k_gate") ? SWE_OK : SWE_CUDA;
 }
 
+const void* run_kernel(int threads, bool link) {
+  if (threads == 128) return link ? (const void*)k_run<128, true> : (const void*)k_run<128, false>;
+  return link ? (const void*)k_run<256, true> : (const void*)k_run<256, false>;
+}
+
+// the run loop as one cooperative launch of the persistent step kernel
+int launch_run(swe_dev_ctx* x) {
+  Dev dcopy = x->d;
+  void* args[] = {&dcopy};
+  CK(cudaLaunchCooperativeKernel(run_kernel(x->tile_threads, x->linked), dim3(x->grid_run),
+                                 dim3(x->tile_threads), args, x->tile_smem, x->stream));
+  ++g_launches;
+  return SWE_OK;
+}
+
 int sync_ctl(swe_dev_ctx* x) {
   CK(cudaMemcpyAsync(x->h_ctl, x->ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, x->stream));
   CK(cudaStreamSynchronize(x->stream));
@@ -237,8 +254,9 @@ int ensure_cfl(swe_dev_ctx* x, bool force = false) {
 // step parameters travel as a kernel argument (captured at launch: no
 // host buffer to race with when launches are only enqueued)
 int write_params(swe_dev_ctx* x, double t_end, long long max_steps, double next_snap,
-                 long long rec_cap, int ring, int mode = 0) {
+                 long long rec_cap, int ring, int mode = 0, long long add_steps = 0) {
   StepParams v;
+  v.add_steps = add_steps;
   v.t_end = t_end;
   v.max_steps = max_steps;
   v.next_snap = next_snap;
@@ -601,6 +619,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_GRAPH_UNROLL")) x->graph_unroll = std::max(1, std::atoi(env));
+  x->persistent = true;  // SWE_PERSISTENT=0: the CUDA-graph loop of k_tile + k_finalize
+  if (const char* env = std::getenv("SWE_PERSISTENT")) x->persistent = std::atoi(env) != 0;
   d.skip = 1;  // dry-tile skipping (fused kernel); SWE_NO_DRY_SKIP=1 turns it off
   if (const char* env = std::getenv("SWE_NO_DRY_SKIP")) d.skip = std::atoi(env) == 0;
   // tile size: 224 cells, a sharp measured optimum on B200 (3-7%
@@ -707,8 +727,19 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     if (!cuda_ok(cudaGetLastError(), "k_pack_cells")) return bail(SWE_CUDA);
   }
   if (!x->fused || d.stage) d.skip = 0;
+  if (!x->fused || d.stage || d.dyn) x->persistent = false;
   if (d.skip)
     if (int rc = build_tile_neighbours(x)) return bail(rc);
+  if (x->persistent) {
+    d.sync = x->alloc<Sync>(1);
+    d.pflag = x->alloc<int>(2 * (size_t)d.ntiles);
+    if (!d.sync || !d.pflag) {
+      g_last_error = "swe_dev_create: cudaMalloc failed";
+      return bail(SWE_CUDA);
+    }
+    cudaMemsetAsync(d.sync, 0, sizeof(Sync), x->stream);
+    cudaMemsetAsync(d.pflag, 0, sizeof(int) * 2 * (size_t)d.ntiles, x->stream);
+  }
   if (d.stage) {  // slot arrays of the staged tile kernel
     const size_t ns = (size_t)E + (size_t)x->n_halo;
     int* soff = x->alloc<int>(d.ntiles + 1);
@@ -763,10 +794,27 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
                            cudaFuncAttributePreferredSharedMemoryCarveout, std::atoi(env));
   }
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_tile, ktile, x->tile_threads, x->tile_smem);
+  if (x->persistent) {
+    int occ_run = 0;
+    for (int L = 0; L < 2; ++L) {
+      int o = 0;
+      if (!cuda_ok(cudaFuncSetAttribute(run_kernel(x->tile_threads, L),
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)x->tile_smem),
+                   "run smem attribute"))
+        return bail(SWE_CUDA);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, run_kernel(x->tile_threads, L),
+                                                    x->tile_threads, x->tile_smem);
+      occ_run = L == 0 ? o : std::min(occ_run, o);
+    }
+    if (occ_run < 1) x->persistent = false;
+    // cooperative launch: every CTA resident at once
+    x->grid_run = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_run)));
+  }
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
   x->grid_tile = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_tile)));
-  d.part = x->alloc<Part>(std::max(x->grid_cell, x->grid_tile));
+  d.part = x->alloc<Part>(std::max(std::max(x->grid_cell, x->grid_tile), x->grid_run));
   if (!d.part) return bail(SWE_CUDA);
 
   Ctl c0{};
@@ -840,6 +888,7 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
     CK(cudaMemsetAsync(x->d.dryflag, 0, sizeof(int) * x->d.ntiles, s));
     CK(cudaMemsetAsync(x->d.skipmask, 0, sizeof(int) * x->d.ntiles, s));
   }
+  if (x->d.pflag) CK(cudaMemsetAsync(x->d.pflag, 0, sizeof(int) * 2 * (size_t)x->d.ntiles, s));
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));
@@ -950,7 +999,10 @@ int swe_dev_advance(swe_dev_ctx* x, double t_end, long long max_steps, double ne
   const long long cap = std::min<long long>(max_records > 0 ? max_records : x->rec_cap, x->rec_cap);
   if (int rc = ensure_cfl(x)) return rc;
   if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
-  if (x->exec) {
+  if (x->persistent) {
+    if (int rc = launch_gate(x)) return rc;
+    if (int rc = launch_run(x)) return rc;
+  } else if (x->exec) {
     CK(cudaGraphLaunch(x->exec, x->stream));
     ++g_launches;
   } else {
@@ -976,10 +1028,15 @@ int swe_dev_advance(swe_dev_ctx* x, double t_end, long long max_steps, double ne
 int swe_dev_advance_async(swe_dev_ctx* x, double t_end, long long max_steps, double next_snap,
                           long long max_records) {
   if (!x) return fail_invalid("null context");
-  if (!x->exec) return fail_invalid("swe_dev_advance_async: context was created without a graph");
+  if (!x->exec && !x->persistent)
+    return fail_invalid("swe_dev_advance_async: context was created without a graph");
   const long long cap = std::min<long long>(max_records > 0 ? max_records : x->rec_cap, x->rec_cap);
   if (int rc = ensure_cfl(x)) return rc;
   if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
+  if (x->persistent) {
+    if (int rc = launch_gate(x)) return rc;
+    return launch_run(x);
+  }
   CK(cudaGraphLaunch(x->exec, x->stream));
   ++g_launches;
   return SWE_OK;
@@ -1000,6 +1057,11 @@ int swe_dev_records(swe_dev_ctx* x, swe_step_record* series, long long max_recor
 int swe_dev_advance_n_async(swe_dev_ctx* x, long long n, double t_end) {
   if (!x) return fail_invalid("null context");
   if (int rc = ensure_cfl(x)) return rc;
+  if (!x->profiling && x->persistent) {  // exactly n steps: the gate sets max_steps = step + n
+    if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, x->rec_cap, 1, 0, n)) return rc;
+    if (int rc = launch_gate(x)) return rc;
+    return launch_run(x);
+  }
   if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, x->rec_cap, 1)) return rc;
   if (int rc = launch_gate(x)) return rc;
   if (x->profiling) {
@@ -1200,11 +1262,11 @@ int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
   if (!x || !out) return fail_invalid("null argument");
   if (n > 11)
     if (int rc = sync_ctl(x)) return rc;
-  const long long v[13] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
+  const long long v[15] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
                            x->grid_tile, x->grid_face, x->grid_cell, (long long)x->tile_smem,
                            x->d.E, x->d.skip, n > 11 ? (long long)x->h_ctl->skipped : 0,
-                           x->graph_unroll};
-  for (int i = 0; i < n && i < 13; ++i) out[i] = v[i];
+                           x->graph_unroll, x->persistent ? 1 : 0, x->grid_run};
+  for (int i = 0; i < n && i < 15; ++i) out[i] = v[i];
   return SWE_OK;
 }
 

@@ -547,6 +547,316 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
 }
 
 // ---------------------------------------------------------------------------
+// persistent step kernel (default run loop).  One cooperative launch steps
+// until the loop stops (t_end, max_steps, snapshot due, record buffer full,
+// error): every CTA owns the same round-robin tiles as k_tile, and the steps
+// are separated by a grid barrier instead of kernel boundaries --
+//   * arrival: each CTA adds one to sync->arrive after its partials; the
+//     LAST to arrive reduces the partials and commits the step exactly as
+//     k_finalize / k_exchange do (same code, same fixed order -> the same
+//     bits), then publishes it as sync->epoch;
+//   * overlap: a CTA does not wait for the commit to start the next step: as
+//     soon as every CTA has arrived (the new state is complete) it decides
+//     its tiles' dry-tile skips and evaluates its first tile's edges -- the
+//     flux needs no dt (engine.hpp:138 takes none) -- and waits for the
+//     epoch (dt, stop) only before the first update.  So the commit, and on a
+//     linked context the whole exchange with the peers, runs behind flux
+//     work.  Linked tiles that read ghost cells wait for the epoch first.
+// Memory model: the state arrays are rewritten during the launch, so they
+// are read with plain (L1-cached, not .nc) loads after an acquire, which
+// invalidates L1 (ld.acquire.gpu -> LDG.STRONG.GPU + CCTL.IVALL on sm_100);
+// dry-tile flags are double-buffered by step parity (pflag) so a flag is
+// never rewritten while another CTA may still read it.
+// Results (state, dt, records, mass, ledger) equal k_tile + k_finalize's bit
+// for bit: the same per-thread tile order, partials and reduction.
+// ---------------------------------------------------------------------------
+constexpr int kRunDec = 128;  // skip decisions held per CTA (recomputed in chunks)
+
+__device__ __forceinline__ bool run_skip(const Dev& d, const int* fl, int t, int tag) {
+  if (__ldcg(fl + t) != tag) return false;
+  const int v0 = __ldg(d.nbr_off + t), v1 = __ldg(d.nbr_off + t + 1);
+  bool ok = true;
+  for (int v = v0; v < v1; ++v) {
+    const int nb = __ldg(d.nbr + v);
+    ok = ok && nb < d.ntiles && __ldcg(fl + nb) == tag;
+  }
+  // a tile whose cells peers hold as ghosts is computed (its pushes run there)
+  if (d.L.nranks > 0 && __ldg(d.L.tile_push + t + 1) > __ldg(d.L.tile_push + t)) ok = false;
+  return ok;
+}
+
+// the last CTA to arrive: reduce the step's partials in the fixed order and
+// commit it (k_finalize / k_exchange's code), then publish the epoch.  Kept
+// out of line: its control-block copies would otherwise cost the step loop
+// registers (ptxas spills).
+template <bool LINK>
+__device__ __noinline__ void run_commit(const Dev& d, Sync* sy, int nb, unsigned epoch,
+                                        Part* scratch) {
+  const Part p = reduce_parts_into(d.part, nb, scratch);  // tile smem is free here
+  if (LINK) {
+    if (threadIdx.x < 32) {
+      post_outcome(d, p, 0);
+      wait_and_commit(d, 0, cudaGraphConditionalHandle{}, 0);
+    }
+  } else if (threadIdx.x == 0) {
+    finalize_local(d, p, cudaGraphConditionalHandle{}, 0);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    st_release_gpu(&sy->epoch, epoch);
+  }
+}
+
+template <int NT, bool LINK>
+__device__ __forceinline__ void run_body(const Dev& d, Sync* sy, const int bid, const int nb) {
+  extern __shared__ double smem[];
+  Ctl* ctl = d.ctl;
+  const int T = d.T;
+  double* sh = smem;
+  double* sq = sh + T;
+  double* sr = sq + T;
+  double* sz = sr + T;
+  double* tm = sz + T;
+  double* tx = tm + 3 * T;
+  double* ty = tx + 3 * T;
+  const Phys P = d.P;
+  __shared__ unsigned char s_dec[kRunDec];
+  __shared__ int s_cur, s_active, s_last;
+  __shared__ long long s_step;
+  __shared__ double s_dt;
+
+  // the committed view of the step a CTA is about to update: published by the
+  // finalizing CTA (epoch >= it), read by thread 0 after the acquire
+  auto read_view = [&](unsigned it) {
+    if (threadIdx.x == 0) {
+      if (it > 0)
+        while (ld_acquire_gpu(&sy->epoch) < it) __nanosleep(20);
+      s_cur = __ldcg(&ctl->cur);
+      s_step = __ldcg(&ctl->step);
+      s_active = __ldcg(&ctl->active);
+      const double t = __ldcg(&ctl->t), dts = __ldcg(&ctl->dts), t_end = __ldcg(&d.sp->t_end);
+      s_dt = (t + dts >= t_end) ? t_end - t : dts;  // engine.hpp:236-237 (step_dt)
+    }
+    __syncthreads();
+    return s_active != 0;
+  };
+  if (!read_view(0)) return;
+  int cur = s_cur;
+  long long step = s_step;
+  double dt = s_dt;
+  const int ntl = bid < d.ntiles ? (d.ntiles - bid + nb - 1) / nb : 0;  // this CTA's tiles
+
+  for (unsigned it = 0;; ++it) {
+    const int tag = (int)(step + 1);
+    const int* fl = d.pflag + (size_t)(step & 1) * d.ntiles;       // flags of this state
+    int* fl_next = d.pflag + (size_t)((step + 1) & 1) * d.ntiles;  // of the next state
+    const double* H = d.h[cur];
+    const double* QX = d.qx[cur];
+    const double* QY = d.qy[cur];
+    double* NH = d.h[cur ^ 1];
+    double* NQX = d.qx[cur ^ 1];
+    double* NQY = d.qy[cur ^ 1];
+    CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
+    bool viewed = it == 0;  // dt / stop of this step known
+    for (int j = 0; j < ntl;) {
+      if (j % kRunDec == 0) {  // skip decisions of the next chunk of tiles
+        __syncthreads();
+        for (int k = threadIdx.x; k < kRunDec && j + k < ntl; k += NT)
+          s_dec[k] = d.skip && run_skip(d, fl, bid + (j + k) * nb, tag);
+        __syncthreads();
+      }
+      const int t = bid + j * nb;
+      const int c0 = t * T;
+      const int nc = min(T, d.C_own - c0);
+      if (s_dec[j % kRunDec]) {
+        // a run of consecutive skipped tiles (as k_tile's fast path): h kept,
+        // q zeroed, mass in tile then cell order; no shared memory
+        int run = 1;
+        while (j + run < ntl && (j + run) % kRunDec != 0 && s_dec[(j + run) % kRunDec]) ++run;
+        if (!viewed) {
+          if (!read_view(it)) return;
+          viewed = true;
+          dt = s_dt;
+        }
+        if (threadIdx.x == 0) {
+          for (int k = 0; k < run; ++k) __stcg(fl_next + t + k * nb, tag + 1);
+          atomicAdd(&ctl->skipped, (unsigned long long)run);
+        }
+        for (int k = 0; k < run; ++k) {
+          const int ck = (t + k * nb) * T;
+          const int nk = min(T, d.C_own - ck);
+          for (int i = threadIdx.x; i < nk; i += NT) {
+            const double h = H[ck + i];
+            NH[ck + i] = h;
+            NQX[ck + i] = 0.0;
+            NQY[ck + i] = 0.0;
+            a.mass += h * __ldg(d.area + ck + i);
+          }
+        }
+        j += run;
+        continue;
+      }
+      // a linked tile that reads ghost cells needs the peers' pushes: the epoch
+      if (LINK && !viewed && __ldg(d.tile_ghost + t)) {
+        if (!read_view(it)) return;
+        viewed = true;
+        dt = s_dt;
+      }
+      for (int i = threadIdx.x; i < nc; i += NT) {
+        sh[i] = H[c0 + i];
+        sq[i] = QX[c0 + i];
+        sr[i] = QY[c0 + i];
+        sz[i] = ldg_geo(d.cg + c0 + i).z;
+      }
+      const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
+      const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
+      __syncthreads();
+      for (int jj = threadIdx.x; jj < ns; jj += NT) {
+        const int e = jj < no ? e0 + jj : __ldg(d.halo + h0 + (jj - no));
+        const int2 ek = __ldg(d.ek + e);
+        const double2 nn = __ldg(d.enxy + e);
+        const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
+        const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
+        const bool w = ek.y == -1;
+        const int il = cl - c0, ir = (w ? cl : cr) - c0;
+        const bool inL = (unsigned)il < (unsigned)nc;
+        Cons uL, uR;
+        double zl, zr;
+        if (inL) {
+          uL = Cons{sh[il], sq[il], sr[il]};
+          zl = sz[il];
+        } else {
+          uL = Cons{H[cl], QX[cl], QY[cl]};
+          zl = __ldg(d.z + cl);
+        }
+        if ((unsigned)ir < (unsigned)nc) {
+          uR = Cons{sh[ir], sq[ir], sr[ir]};
+          zr = sz[ir];
+        } else {
+          const int c = ir + c0;
+          uR = Cons{H[c], QX[c], QY[c]};
+          zr = __ldg(d.z + c);
+        }
+        if (uL.h < 0.0 || (!w && uR.h < 0.0)) {  // engine.hpp:147-153
+          atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
+          continue;
+        }
+        const double hg = 0.5 * P.g;
+        const int sl = 3 * il + (int)((unsigned)ek.x >> 30);
+        if (!w) {
+          double f0, lx, ly, rx, ry;
+          interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
+          const int2 ek2 = __ldg(d.ek + e);
+          const double len2 = __ldg(d.len + e);
+          const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
+          if ((unsigned)il2 < (unsigned)nc) {
+            const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
+            const double ownL = (hg * uL.h) * uL.h;
+            tm[s2] = f0 * len2;
+            tx[s2] = (lx - ownL * nx) * len2;
+            ty[s2] = (ly - ownL * ny) * len2;
+          }
+          if ((unsigned)ir2 < (unsigned)nc) {
+            const int s3 = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
+            const double ownR = (hg * uR.h) * uR.h;
+            tm[s3] = (-f0) * len2;
+            tx[s3] = (rx - ownR * (-nx)) * len2;
+            ty[s3] = (ry - ownR * (-ny)) * len2;
+          }
+        } else if (inL) {
+          const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
+          const double ownL = (hg * uL.h) * uL.h;
+          tm[sl] = f.m * len;
+          tx[sl] = (f.fx - ownL * nx) * len;
+          ty[sl] = (f.fy - ownL * ny) * len;
+        }
+      }
+      __syncthreads();
+      if (!viewed) {  // the first computed tile's edges are done: now dt / stop
+        if (!read_view(it)) return;
+        viewed = true;
+        dt = s_dt;
+      }
+      int p0 = 0, p1 = 0;
+      if (LINK) {
+        p0 = __ldg(d.L.tile_push + t);
+        p1 = __ldg(d.L.tile_push + t + 1);
+      }
+      int dry = 1;
+      for (int i = threadIdx.x; i < nc; i += NT) {
+        double am = 0.0, ax = 0.0, ay = 0.0;  // engine.hpp:255-264, local order k
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+          am += tm[3 * i + k];
+          ax += tx[3 * i + k];
+          ay += ty[3 * i + k];
+        }
+        const CellGeo g = ldg_geo(d.cg + c0 + i);
+        const Cons u = cell_finish_v(d, c0 + i, sh[i], sq[i], sr[i], am, ax, ay, dt, g.area, g.man,
+                                     g.inr, NH, NQX, NQY, a);
+        dry &= (0.0 <= u.h && u.h < P.h_dry) ? 1 : 0;
+        if (LINK && p1 > p0) {
+          sh[i] = u.h;
+          sq[i] = u.qx;
+          sr[i] = u.qy;
+        }
+      }
+      dry = __syncthreads_and(dry);
+      if (threadIdx.x == 0 && d.skip) __stcg(fl_next + t, dry ? tag + 1 : 0);
+      if (LINK && p1 > p0) {
+        for (int q = p0 + threadIdx.x; q < p1; q += NT) {
+          const int i = __ldg(d.L.push_cell + q) - c0, g = __ldg(d.L.push_ghost + q);
+          double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + q) + 3 * (cur ^ 1);
+          dst[0][g] = sh[i];
+          dst[1][g] = sq[i];
+          dst[2][g] = sr[i];
+        }
+        __threadfence_system();
+        __syncthreads();
+      }
+      ++j;
+    }
+    if (!viewed) {  // a CTA without tiles still follows the loop
+      if (!read_view(it)) return;
+      viewed = true;
+    }
+    block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + bid);
+    // arrive; the last CTA commits the step (k_finalize / k_exchange's code)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      const unsigned old = atomicAdd(&sy->arrive, 1u);
+      s_last = old + 1 == (unsigned)nb * (it + 1);
+      if (s_last) __threadfence();
+    }
+    __syncthreads();
+    if (s_last) run_commit<LINK>(d, sy, nb, it + 1, reinterpret_cast<Part*>(smem));
+    // every CTA has arrived: the next state and its dry-tile flags are complete
+    if (threadIdx.x == 0)
+      while (ld_acquire_gpu(&sy->arrive) < (unsigned)nb * (it + 1)) __nanosleep(20);
+    __syncthreads();
+    cur ^= 1;  // the next step, provisionally (confirmed by its epoch)
+    step += 1;
+  }
+}
+
+template <int NT, bool LINK>
+__global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d) {
+  run_body<NT, LINK>(d, d.sync, blockIdx.x, gridDim.x);
+}
+
+// P linked ranks' persistent kernels as ONE cooperative launch on one device
+// (blocks [r G, (r+1) G) run rank r): the ranks' CTAs spin on each other's
+// mailboxes truly concurrently, which separate launches sharing a device
+// cannot guarantee.  Test path for the linked exchange (B200_PROFILING.md).
+template <int NT>
+__global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run_ranks(const Dev* devs, int G) {
+  const Dev& d = devs[blockIdx.x / G];
+  run_body<NT, true>(d, d.sync, blockIdx.x % G, G);
+}
+
+// ---------------------------------------------------------------------------
 // staged tile kernel (option, SWE_TILE_STAGE=1): every contiguous input of a
 // tile -- state, bed, area, n, r of its cells and the per-tile slot arrays
 // (owned + halo edges copied in tile order at create) -- is brought into

@@ -7,9 +7,10 @@
   max speed and clip events;
 * BASELINE config [1] (1,058,000-cell three-mound flood, Manning n = 0.03)
   over 3000 steps against the reference: bit-identical (friction included);
-* BASELINE config [4] at its largest rung (the nx = 6406 square, 82,076,872
-  cells): 8 linked parts in lockstep on one GPU equal the single-domain run
-  over 20 steps (the single-domain path is pinned to the reference above).
+* BASELINE config [4] at its largest rung (the nx = 6406 square,
+  2 x 6406^2 = 82,073,672 cells; SURVEY.md §8(a) prints 82,076,872): 8
+  linked parts in lockstep on one GPU equal the single-domain run over 20
+  steps (the single-domain path is pinned to the reference above).
 """
 import os
 
@@ -78,7 +79,7 @@ def test_weak_square_82M_eight_linked_parts_match_single_domain():
     sc = api.make_scenario("weak_square", weak_nx=6406)
     mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
     C = mesh.n_cells
-    assert C == 82_076_872
+    assert C == 2 * 6406 * 6406  # 82,073,672
     s = api.DeviceSolver(mesh)
     s.set_state(sc.state)
     ref_recs = s.advance(1e30, max_steps=20)
