@@ -314,7 +314,9 @@ def run_b200_dist(args, rank, local, world):
                                                                   parts=world))
     lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
-    U = api.DeviceSolver.info(lp)["graph_unroll"]  # steps per WHILE iteration
+    inf = api.DeviceSolver.info(lp)
+    U = inf["graph_unroll"]  # steps per WHILE iteration (graph loop)
+    PERSISTENT = bool(inf["persistent"])
     try:
         dist.link_torch(lp)
     except dist.LinkUnavailable as e:  # every rank takes this branch together
@@ -417,11 +419,15 @@ def run_b200_dist(args, rank, local, world):
                    "cells_per_gpu_min": int(np.bincount(part).min()),
                    "halo_cells_rank0": int(lm.n_cells - lm.n_owned)},
                "setup": {"setup_s": round(setup_s, 2)},
-               "gpu_launches": 2 * U * -(-K // U) + 2,
-               "gpu_launches_note": "per rank: k_set_params + one CUDA-graph launch = k_gate + "
-                                    f"a conditional WHILE node of ceil(K/{U}) iterations x {U} x "
-                                    "(k_tile with halo push, k_exchange); steps past the stop "
-                                    "exit at once",
+               "gpu_launches": 3 if PERSISTENT else 2 * U * -(-K // U) + 2,
+               "gpu_launches_note": ("per rank: k_set_params, k_gate and one cooperative launch "
+                                     "of the persistent step kernel (halo pushed peer-to-peer by "
+                                     "the tiles, the exchange run by the last CTA to arrive while "
+                                     "the others start the next step's fluxes)" if PERSISTENT else
+                                     "per rank: k_set_params + one CUDA-graph launch = k_gate + "
+                                     f"a conditional WHILE node of ceil(K/{U}) iterations x {U} x "
+                                     "(k_tile with halo push, k_exchange); steps past the stop "
+                                     "exit at once"),
                "clocks": clk.summary() if clk else None,
                "roofline": dist_roofline(mesh, K, ms, world, skip_frac),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
@@ -678,14 +684,19 @@ def run_b200(args):
            "config": workload_config(args.config, C, E, mesh.n_boundary_edges, world),
            "setup": {"setup_s": round(setup_s, 2), "create_s": round(create_s, 2),
                      "device_bytes": solver.memory_bytes()},
-           "gpu_launches": (2 if info["fused"] else 3) * info["graph_unroll"]
-                           * -(-K // info["graph_unroll"]) + 2,
-           "gpu_launches_note": "k_set_params + one CUDA-graph launch = k_gate + a conditional "
-                                f"WHILE node of ceil(K/{info['graph_unroll']}) iterations x "
-                                f"{info['graph_unroll']} x ("
-                                + ("k_tile" if info["fused"] else "k_face_c, k_cell_c")
-                                + ", k_finalize); steps past the stop exit at once "
-                                f"(host-side launch calls: {launches})",
+           "gpu_launches": (3 if info["persistent"] else
+                            (2 if info["fused"] else 3) * info["graph_unroll"]
+                            * -(-K // info["graph_unroll"]) + 2),
+           "gpu_launches_note": ("k_set_params, k_gate and ONE cooperative launch of the "
+                                 f"persistent step kernel k_run ({info['grid_run']} CTAs) for all "
+                                 f"{K} steps (grid barrier per step; the last CTA to arrive "
+                                 "commits the step)" if info["persistent"] else
+                                 "k_set_params + one CUDA-graph launch = k_gate + a conditional "
+                                 f"WHILE node of ceil(K/{info['graph_unroll']}) iterations x "
+                                 f"{info['graph_unroll']} x ("
+                                 + ("k_tile" if info["fused"] else "k_face_c, k_cell_c")
+                                 + ", k_finalize); steps past the stop exit at once")
+                                + f" (host-side launch calls: {launches})",
            "roofline": roof,
            "clocks": clk.summary()}
     if info["fused"]:

@@ -220,6 +220,14 @@ SWE_API int swe_dev_link(swe_dev_ctx* ctx, int rank, int nranks, void* const* ar
  * 0 open, 1 CFL wait + gate, 2 step kernel + halo push, 3 post, 4 wait +
  * commit.  Run phase k on every context before phase k+1 on any. */
 SWE_API int swe_dev_link_phase(swe_dev_ctx* ctx, int phase, double t_end);
+/* P linked contexts (ranks 0..P-1, persistent kernel, all on ONE device)
+ * stepped nsteps steps by ONE cooperative launch of the persistent step
+ * kernel: the ranks' CTAs run concurrently and exchange through the device
+ * mailboxes as on P GPUs (separate launches that wait on each other must not
+ * share a device).  grid: CTAs per rank (0 = as many as fit).  Test path for
+ * the concurrent exchange protocol; returns the first rank's error status. */
+SWE_API int swe_dev_run_ranks(swe_dev_ctx* const* ctxs, int n, long long nsteps, double t_end,
+                              int grid);
 /* Status and record of the last single step (after phase 4). */
 SWE_API int swe_dev_last_record(swe_dev_ctx* ctx, swe_step_record* rec, swe_status* st);
 
@@ -233,7 +241,8 @@ SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launch
  * tile, [4] halo edges, [5] tile grid, [6] face grid, [7] cell grid,
  * [8] tile shared-memory bytes, [9] edges, [10] dry-tile skipping on?,
  * [11] dry tiles skipped so far (n > 11 synchronises the context),
- * [12] steps per WHILE iteration of the run graph. */
+ * [12] steps per WHILE iteration of the run graph, [13] run loop is the
+ * persistent kernel?, [14] its CTAs. */
 SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
 
 /* Per cell (reference numbering): 1 if dry-tile skipping will skip the cell's

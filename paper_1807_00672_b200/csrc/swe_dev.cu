@@ -95,6 +95,7 @@ struct swe_dev_ctx {
   bool cfl_host_valid = false;  // the device CFL cache is known valid (no sync needed)
   int graph_unroll = 8;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
   bool persistent = false;      // run loop = one cooperative k_run launch (SWE_PERSISTENT=0: graph)
+  Dev* d_dev = nullptr;         // device copy of d for k_run's commit path
   int grid_run = 0;             // CTAs of k_run (= grid_tile when the occupancies agree)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
@@ -217,7 +218,10 @@ const void* run_kernel(int threads, bool link) {
 // the run loop as one cooperative launch of the persistent step kernel
 int launch_run(swe_dev_ctx* x) {
   Dev dcopy = x->d;
-  void* args[] = {&dcopy};
+  // the commit path reads the context's Dev from global memory (stream-ordered copy)
+  CK(cudaMemcpyAsync(x->d_dev, &x->d, sizeof(Dev), cudaMemcpyHostToDevice, x->stream));
+  const Dev* dg = x->d_dev;
+  void* args[] = {&dcopy, &dg};
   CK(cudaLaunchCooperativeKernel(run_kernel(x->tile_threads, x->linked), dim3(x->grid_run),
                                  dim3(x->tile_threads), args, x->tile_smem, x->stream));
   ++g_launches;
@@ -733,7 +737,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   if (x->persistent) {
     d.sync = x->alloc<Sync>(1);
     d.pflag = x->alloc<int>(2 * (size_t)d.ntiles);
-    if (!d.sync || !d.pflag) {
+    x->d_dev = x->alloc<Dev>(1);
+    if (!d.sync || !d.pflag || !x->d_dev) {
       g_last_error = "swe_dev_create: cudaMalloc failed";
       return bail(SWE_CUDA);
     }
@@ -810,6 +815,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     if (occ_run < 1) x->persistent = false;
     // cooperative launch: every CTA resident at once
     x->grid_run = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_run)));
+    if (const char* env = std::getenv("SWE_RUN_GRID"))  // test hook: fewer CTAs, more tiles each
+      x->grid_run = std::max(1, std::min(x->grid_run, std::atoi(env)));
   }
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
@@ -1387,6 +1394,14 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
   d.L = L;
   x->n_push = n_push;
   x->linked = true;
+  if (x->persistent) {  // tiles whose edges read ghost cells wait for the exchange
+    unsigned char* tg = nullptr;
+    CK(cudaMalloc(&tg, std::max(1, d.ntiles)));
+    x->link_allocs.push_back(tg);
+    k_tile_ghost<<<blocks_for(d.ntiles), kBlock, 0, x->stream>>>(d, tg);
+    CK(cudaGetLastError());
+    d.tile_ghost = tg;
+  }
   // the CFL cache must be re-formed globally; the graph gains the exchange
   if (int rc = sync_ctl(x)) return rc;
   // every rank starts linked with its current state in buffer 0 and no
@@ -1447,6 +1462,78 @@ int swe_dev_link_phase(swe_dev_ctx* x, int phase, double t_end) {
     case 4: return launch_wait(x, 0, cudaGraphConditionalHandle{}, 0);
   }
   return fail_invalid("swe_dev_link_phase: phase must be 0..4");
+}
+
+// P linked contexts sharing ONE device stepped by one cooperative launch of
+// the persistent kernel (k_run_ranks): the ranks' CTAs run concurrently and
+// exchange through the mailboxes exactly as on P GPUs.  Test path: separate
+// launches that wait on each other must not share a device.
+int swe_dev_run_ranks(swe_dev_ctx* const* xs, int n, long long nsteps, double t_end, int grid) {
+  if (!xs || n < 1 || nsteps < 1) return fail_invalid("swe_dev_run_ranks: bad argument");
+  int G = grid > 0 ? grid : INT_MAX;
+  for (int r = 0; r < n; ++r) {
+    swe_dev_ctx* x = xs[r];
+    if (!x || !x->linked || !x->persistent || x->device != xs[0]->device ||
+        x->tile_threads != xs[0]->tile_threads || x->d.L.rank != r || x->d.L.nranks != n)
+      return fail_invalid("swe_dev_run_ranks: contexts must be persistent, linked as ranks "
+                          "0..n-1 of n, on one device");
+    G = std::min(G, std::min(x->d.ntiles, x->grid_run));
+  }
+  const int NT = xs[0]->tile_threads;
+  size_t smem = 0;
+  for (int r = 0; r < n; ++r) smem = std::max(smem, xs[r]->tile_smem);
+  const void* kr = NT == 128 ? (const void*)k_run_ranks<128> : (const void*)k_run_ranks<256>;
+  CK(cudaSetDevice(xs[0]->device));
+  CK(cudaFuncSetAttribute(kr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int occ = 0, sms = 148;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, xs[0]->device));
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kr, NT, smem));
+  G = std::min(G, sms * occ / n);
+  if (G < 1) return fail_invalid("swe_dev_run_ranks: too many ranks for one device");
+  // CFL bound of the current state: every rank posts, then every rank waits
+  // (phases, so no waiting kernel runs before all posts are done)
+  std::vector<bool> posted(n, false);
+  for (int r = 0; r < n; ++r) {
+    swe_dev_ctx* x = xs[r];
+    if (int rc = sync_ctl(x)) return rc;
+    if (!x->h_ctl->cfl_valid) {
+      k_cfl<<<x->grid_cell, kBlock, 0, x->stream>>>(x->d);
+      ++g_launches;
+      if (int rc = launch_post(x, x->grid_cell, 1)) return rc;
+      posted[r] = true;
+    }
+  }
+  for (int r = 0; r < n; ++r) CK(cudaStreamSynchronize(xs[r]->stream));
+  for (int r = 0; r < n; ++r)
+    if (posted[r])
+      if (int rc = launch_wait(xs[r], 1, cudaGraphConditionalHandle{}, 0)) return rc;
+  for (int r = 0; r < n; ++r) {
+    swe_dev_ctx* x = xs[r];
+    x->cfl_host_valid = true;
+    if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, x->rec_cap, 1, 0, nsteps)) return rc;
+    if (int rc = launch_gate(x)) return rc;
+  }
+  std::vector<Dev> devs(n);
+  for (int r = 0; r < n; ++r) devs[r] = xs[r]->d;
+  Dev* ddevs = nullptr;
+  CK(cudaMalloc(&ddevs, sizeof(Dev) * n));
+  struct Free {
+    void* p;
+    ~Free() { cudaFree(p); }
+  } guard{ddevs};
+  CK(cudaMemcpy(ddevs, devs.data(), sizeof(Dev) * n, cudaMemcpyHostToDevice));
+  for (int r = 0; r < n; ++r) CK(cudaStreamSynchronize(xs[r]->stream));
+  const Dev* dp = ddevs;
+  void* args[] = {&dp, &G};
+  CK(cudaLaunchCooperativeKernel(kr, dim3(G * n), dim3(NT), args, smem, xs[0]->stream));
+  ++g_launches;
+  CK(cudaStreamSynchronize(xs[0]->stream));
+  int worst = SWE_OK;
+  for (int r = 0; r < n; ++r) {
+    const int code = read_status(xs[r], nullptr);
+    if (code != SWE_OK && worst == SWE_OK) worst = code;
+  }
+  return worst;
 }
 
 int swe_dev_last_record(swe_dev_ctx* x, swe_step_record* rec, swe_status* st) {

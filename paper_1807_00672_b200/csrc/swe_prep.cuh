@@ -419,6 +419,20 @@ __global__ void k_point(int kind, long long n, Phys P, const double* l, const do
   }
 }
 
+// linked contexts: tiles with an edge on a ghost cell (they read peers' pushes)
+__global__ void k_tile_ghost(Dev d, unsigned char* out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= d.ntiles) return;
+  int g = 0;
+  auto touch = [&](int e) {
+    const int r = d.er[e];
+    g |= d.el[e] >= d.C_own || r >= d.C_own;
+  };
+  for (int e = d.eoff[t]; e < d.eoff[t + 1]; ++e) touch(e);
+  for (int k = d.hoff[t]; k < d.hoff[t + 1]; ++k) touch(d.halo[k]);
+  out[t] = (unsigned char)g;
+}
+
 // total_mass (engine.hpp:128-132) of host arrays: a fixed-order tree sum
 // (gridDim.x partials, each a fixed strided walk + shuffle tree; then one
 // block folds the partials), independent of the device it runs on

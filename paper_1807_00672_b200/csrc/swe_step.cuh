@@ -590,8 +590,9 @@ __device__ __forceinline__ bool run_skip(const Dev& d, const int* fl, int t, int
 // out of line: its control-block copies would otherwise cost the step loop
 // registers (ptxas spills).
 template <bool LINK>
-__device__ __noinline__ void run_commit(const Dev& d, Sync* sy, int nb, unsigned epoch,
+__device__ __noinline__ void run_commit(const Dev* dg, Sync* sy, int nb, unsigned epoch,
                                         Part* scratch) {
+  const Dev& d = *dg;  // the context's Dev in global memory (no local copy of the parameter)
   const Part p = reduce_parts_into(d.part, nb, scratch);  // tile smem is free here
   if (LINK) {
     if (threadIdx.x < 32) {
@@ -609,7 +610,8 @@ __device__ __noinline__ void run_commit(const Dev& d, Sync* sy, int nb, unsigned
 }
 
 template <int NT, bool LINK>
-__device__ __forceinline__ void run_body(const Dev& d, Sync* sy, const int bid, const int nb) {
+__device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, const int bid,
+                                         const int nb) {
   extern __shared__ double smem[];
   Ctl* ctl = d.ctl;
   const int T = d.T;
@@ -831,7 +833,7 @@ __device__ __forceinline__ void run_body(const Dev& d, Sync* sy, const int bid, 
       if (s_last) __threadfence();
     }
     __syncthreads();
-    if (s_last) run_commit<LINK>(d, sy, nb, it + 1, reinterpret_cast<Part*>(smem));
+    if (s_last) run_commit<LINK>(dg, sy, nb, it + 1, reinterpret_cast<Part*>(smem));
     // every CTA has arrived: the next state and its dry-tile flags are complete
     if (threadIdx.x == 0)
       while (ld_acquire_gpu(&sy->arrive) < (unsigned)nb * (it + 1)) __nanosleep(20);
@@ -842,8 +844,8 @@ __device__ __forceinline__ void run_body(const Dev& d, Sync* sy, const int bid, 
 }
 
 template <int NT, bool LINK>
-__global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d) {
-  run_body<NT, LINK>(d, d.sync, blockIdx.x, gridDim.x);
+__global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d, const Dev* dg) {
+  run_body<NT, LINK>(d, dg, d.sync, blockIdx.x, gridDim.x);
 }
 
 // P linked ranks' persistent kernels as ONE cooperative launch on one device
@@ -853,7 +855,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d) {
 template <int NT>
 __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run_ranks(const Dev* devs, int G) {
   const Dev& d = devs[blockIdx.x / G];
-  run_body<NT, true>(d, d.sync, blockIdx.x % G, G);
+  run_body<NT, true>(d, &d, d.sync, blockIdx.x % G, G);
 }
 
 // ---------------------------------------------------------------------------

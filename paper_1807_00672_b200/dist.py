@@ -588,6 +588,24 @@ def run_lockstep(parts, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 5)
 
 
+def run_ranks(parts, nsteps: int, t_end: float = 1e30, grid: int = 0):
+    """Step linked parts of ONE process on ONE device concurrently: one
+    cooperative launch of the persistent step kernel over all ranks
+    (swe_dev_run_ranks), so the ranks' exchange runs as it does on P GPUs
+    (no lockstep phases).  Returns the records of the last nsteps steps."""
+    nr = len(parts)
+    by_rank = sorted(parts, key=lambda p: p.lm.part)
+    arr = (C.c_void_p * nr)(*[p.ctx.value for p in by_rank])
+    rc = by_rank[0].lib.swe_dev_run_ranks(arr, nr, nsteps, t_end, grid)
+    recs = [p.records() for p in by_rank]  # raises the rank's error, if any
+    if rc:
+        _check(rc, "swe_dev_run_ranks")
+    for r in recs[1:]:
+        if not np.array_equal(r, recs[0]):
+            raise RuntimeError("linked ranks disagree on the step records")
+    return recs[0][-nsteps:]
+
+
 def run_lockstep_ranks(part: LinkedPart, nsteps: int, t_end: float = 1e30, group=None):
     """run_lockstep across processes: a torch.distributed barrier between
     phases, so every rank's post precedes every rank's wait (debug driver
@@ -629,4 +647,4 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
 
 __all__ = ["partition", "cost_weights", "measured_cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
-           "run_lockstep", "DeviceError", "LinkUnavailable"]
+           "run_lockstep", "run_ranks", "DeviceError", "LinkUnavailable"]
