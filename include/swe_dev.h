@@ -91,7 +91,8 @@ typedef struct {
 
 /* create flags */
 #define SWE_FLAG_IDENTITY_ORDER 1u /* skip the Morton renumbering */
-#define SWE_FLAG_NO_GRAPH 2u       /* advance with plain launches, no CUDA graph */
+#define SWE_FLAG_NO_GRAPH 2u       /* advance with plain launches: no CUDA graph and no
+                                      persistent step kernel */
 #define SWE_FLAG_TWO_PHASE 4u      /* face kernel + cell kernel (records through HBM)
                                       instead of the fused tile kernel */
 

@@ -279,48 +279,52 @@ __global__ void __launch_bounds__(kBlock) k_cfl(Dev d) {
   block_reduce_part(lo, hi, mass, 0.0, 0, d.part + blockIdx.x);
 }
 
-// fixed-order reduction of n block partials by one block; s: blockDim.x
-// Parts of shared scratch.  Loads bypass L1 (the partials were written by
-// other SMs of the same launch when called from a step kernel's last block).
+// fixed-order reduction of n block partials by one block: a tree of kBlock
+// virtual lanes whatever blockDim.x is (k_finalize runs 256 threads, the
+// persistent kernel's committing CTA 128), so every path forms the same sums
+// in the same order; s: kBlock Parts of shared scratch.  Loads bypass L1 (the
+// partials were written by other SMs of the same launch when called from a
+// step kernel's last block).
 __device__ Part reduce_parts_into(const Part* part, int n, Part* s) {
-  Part p{INFINITY, 0.0, 0.0, 0.0, 0, 0};
-  const int bd = blockDim.x;
-  for (int base = threadIdx.x; base < n; base += 8 * bd) {
-    Part q[8];  // 8 independent loads in flight, folded in index order
+  for (int v = threadIdx.x; v < kBlock; v += blockDim.x) {
+    Part p{INFINITY, 0.0, 0.0, 0.0, 0, 0};
+    for (int base = v; base < n; base += 8 * kBlock) {
+      Part q[8];  // 8 independent loads in flight, folded in index order
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int i = base + k * bd;
-      if (i < n) {
-        q[k].lo = __ldcg(&part[i].lo);
-        q[k].hi = __ldcg(&part[i].hi);
-        q[k].mass = __ldcg(&part[i].mass);
-        q[k].clip = __ldcg(&part[i].clip);
-        q[k].events = __ldcg(&part[i].events);
+      for (int k = 0; k < 8; ++k) {
+        const int i = base + k * kBlock;
+        if (i < n) {
+          q[k].lo = __ldcg(&part[i].lo);
+          q[k].hi = __ldcg(&part[i].hi);
+          q[k].mass = __ldcg(&part[i].mass);
+          q[k].clip = __ldcg(&part[i].clip);
+          q[k].events = __ldcg(&part[i].events);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        if (base + k * kBlock < n) {
+          p.lo = sel_min(p.lo, q[k].lo);
+          p.hi = sel_max(p.hi, q[k].hi);
+          p.mass += q[k].mass;
+          p.clip += q[k].clip;
+          p.events += q[k].events;
+        }
       }
     }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (base + k * bd < n) {
-        p.lo = sel_min(p.lo, q[k].lo);
-        p.hi = sel_max(p.hi, q[k].hi);
-        p.mass += q[k].mass;
-        p.clip += q[k].clip;
-        p.events += q[k].events;
-      }
-    }
+    s[v] = p;
   }
-  s[threadIdx.x] = p;
   __syncthreads();
-  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-    if (threadIdx.x < o) {
-      Part a = s[threadIdx.x];
-      const Part b = s[threadIdx.x + o];
+  for (int o = kBlock / 2; o > 0; o >>= 1) {
+    for (int v = threadIdx.x; v < o; v += blockDim.x) {
+      Part a = s[v];
+      const Part b = s[v + o];
       a.lo = sel_min(a.lo, b.lo);
       a.hi = sel_max(a.hi, b.hi);
       a.mass += b.mass;
       a.clip += b.clip;
       a.events += b.events;
-      s[threadIdx.x] = a;
+      s[v] = a;
     }
     __syncthreads();
   }

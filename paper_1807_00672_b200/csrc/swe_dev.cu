@@ -731,7 +731,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
     if (!cuda_ok(cudaGetLastError(), "k_pack_cells")) return bail(SWE_CUDA);
   }
   if (!x->fused || d.stage) d.skip = 0;
-  if (!x->fused || d.stage || d.dyn) x->persistent = false;
+  // plain launches (SWE_FLAG_NO_GRAPH) keep the one-kernel-per-phase path
+  if (!x->fused || d.stage || d.dyn || (flags & SWE_FLAG_NO_GRAPH)) x->persistent = false;
   if (d.skip)
     if (int rc = build_tile_neighbours(x)) return bail(rc);
   if (x->persistent) {
@@ -779,6 +780,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_face, k_face_c, kBlock, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cell, k_cell_c, kBlock, 0);
   x->tile_smem = d.stage ? tile_stage_smem_bytes(d.T, d.max_slots) : tile_smem_bytes(d.T, d.max_slots);
+  if (x->persistent)  // k_run's commit reduces the partials in the tile's shared memory
+    x->tile_smem = std::max(x->tile_smem, (size_t)kBlock * sizeof(Part));
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if ((long long)x->tile_smem + 1024 > smem_optin) {
