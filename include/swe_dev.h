@@ -225,10 +225,16 @@ SWE_API int swe_dev_link_phase(swe_dev_ctx* ctx, int phase, double t_end);
  * stepped nsteps steps by ONE cooperative launch of the persistent step
  * kernel: the ranks' CTAs run concurrently and exchange through the device
  * mailboxes as on P GPUs (separate launches that wait on each other must not
- * share a device).  grid: CTAs per rank (0 = as many as fit).  Test path for
+ * share a device).  grid: CTAs per rank, one of them the rank's control block
+ * (0 = as many as fit).  Test path for
  * the concurrent exchange protocol; returns the first rank's error status. */
 SWE_API int swe_dev_run_ranks(swe_dev_ctx* const* ctxs, int n, long long nsteps, double t_end,
                               int grid);
+/* Experiment builds (-DSWE_RUN_TIMING=1): phase-time sums of the persistent
+ * step kernel [worker work ns, worker epoch-wait ns, control wait for the
+ * arrivals ns, commit ns, worker CTA-steps, commits, worker arrival-wait ns],
+ * read and cleared (zeros in normal builds). */
+SWE_API int swe_dev_run_timing(swe_dev_ctx* ctx, long long* out, int n);
 /* Status and record of the last single step (after phase 4). */
 SWE_API int swe_dev_last_record(swe_dev_ctx* ctx, swe_step_record* rec, swe_status* st);
 

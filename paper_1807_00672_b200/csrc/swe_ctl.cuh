@@ -114,7 +114,12 @@ struct Link {
 struct __align__(128) Sync {
   unsigned int arrive;
   unsigned int epoch;
-  unsigned int pad[30];
+  // the step's CFL bound and max speed (bits of non-negative doubles, so
+  // integer atomicMin / atomicMax order them exactly), double-buffered by
+  // step parity: min and max are order-independent, so the workers fold them
+  // in at arrival and the commit needs no reduction on its critical path
+  unsigned long long lo[2], hi[2];
+  unsigned long long timing[12];  // SWE_RUN_TIMING builds
 };
 
 struct __align__(32) CellGeo {
@@ -202,6 +207,33 @@ __device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
   return v;
 }
 
+// relaxed (no L1 invalidation) poll; acquire fence (MEMBAR + CCTL.IVALL on
+// sm_100) once the value is seen; release atomic add (MEMBAR, no IVALL)
+__device__ __forceinline__ unsigned int ld_relaxed_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// wait until *p >= v: relaxed polls with exponential back-off (every CTA's
+// thread 0 polls the same line; 20 ns polls made ~6M L2 requests per step
+// at 10M cells and slowed every CTA's L2 traffic)
+__device__ __forceinline__ void poll_until(const unsigned int* p, unsigned int v) {
+  unsigned int ns = 32;
+  while (ld_relaxed_gpu(p) < v) {
+    __nanosleep(ns);
+    ns = ns < 1024 ? 2 * ns : 1024;
+  }
+}
+
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+__device__ __forceinline__ unsigned int atom_add_release_gpu(unsigned int* p, unsigned int v) {
+  unsigned int old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
@@ -252,6 +284,19 @@ __device__ __forceinline__ void block_reduce_part(double lo, double hi, double m
     }
     *out = p;
   }
+}
+
+// block_reduce_part that also hands the block's partial to thread 0
+__device__ __forceinline__ Part block_reduce_part_ret(double lo, double hi, double mass, double clip,
+                                                      long long ev, Part* out) {
+  __shared__ Part s_p;
+  block_reduce_part(lo, hi, mass, clip, ev, &s_p);
+  Part p{};
+  if (threadIdx.x == 0) {
+    p = s_p;
+    *out = p;
+  }
+  return p;
 }
 
 // standalone CFL + mass of the current state (first step after set_state),
@@ -366,6 +411,10 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   if (d.sync) {  // the persistent kernel's barrier starts over with every launch
     d.sync->arrive = 0;
     d.sync->epoch = 0;
+    for (int k = 0; k < 2; ++k) {
+      d.sync->lo[k] = 0x7ff0000000000000ULL;  // +inf
+      d.sync->hi[k] = 0ULL;                   // +0
+    }
   }
   c->tile_next = 0;
   c->bad_edge = kNone;
@@ -400,16 +449,55 @@ __device__ __forceinline__ Ctl load_ctl(const Ctl* c) {
   return v;
 }
 
+// write back the fields the committing thread owns.  The error slots
+// bad_edge / bad_cell and the counters (skipped) are left alone: in the
+// persistent kernel other CTAs may already be evaluating the next step's
+// fluxes and atomicMin-ing bad_edge while the step is committed (a slot is
+// only ever set by a failing step, which stops the loop; k_gate clears them)
+__device__ __forceinline__ void store_commit(Ctl* g, const Ctl& c) {
+  g->t = c.t;
+  g->step = c.step;
+  g->clipped = c.clipped;
+  g->events = c.events;
+  g->dts = c.dts;
+  g->max_speed = c.max_speed;
+  g->mass = c.mass;
+  g->cfl_valid = c.cfl_valid;
+  g->cfl_bad = c.cfl_bad;
+  g->cur = c.cur;
+  g->n_rec = c.n_rec;
+  g->status = c.status;
+  g->err_index = c.err_index;
+  g->err_step = c.err_step;
+  g->err_dt = c.err_dt;
+  g->err_h = c.err_h;
+  g->bad_speed = c.bad_speed;
+  g->tile_next = c.tile_next;
+  g->active = c.active;
+}
+
 // engine.hpp:292-307 + the fused CFL cache for the next step, given the
 // step's reduced partials p and outcome (status, index, err_h).  One thread;
 // works on a register copy of the control block (one batch of loads).
-__device__ void finalize_step(const Dev& d, const Part& p, int status, int index, double err_h,
-                              cudaGraphConditionalHandle cond, int use_cond) {
-  Ctl c = load_ctl(d.ctl);
+// the commit arithmetic on a control-block copy c (no global loads), in two
+// parts: commit_head -- everything the NEXT step depends on (clock, buffer,
+// CFL bound from the min / max lo, hi, stop decision) -- and commit_tail --
+// the fixed-order sums (mass, clip ledger) and the step's record, which
+// nothing in the next step reads.  k_finalize runs both back to back; the
+// persistent kernel's control block publishes the step after the head.
+struct CommitInfo {
+  long long slot, step;
+  double t, dt, max_speed_pre;
+  int ok;
+};
+
+__device__ __forceinline__ int commit_head(Ctl& c, const StepParams& sp, double lo, double hi,
+                                           int status, int index, double err_h, const Phys& P,
+                                           CommitInfo& ci) {
   c.tile_next = 0;
-  const StepParams sp = *d.sp;
   const bool last = c.t + c.dts >= sp.t_end;  // engine.hpp:236-237
   const double dt = last ? sp.t_end - c.t : c.dts;
+  ci.ok = status == SWE_OK;
   if (status != SWE_OK) {  // engine.hpp:168-169, :292-297; state is not committed
     c.status = status;
     c.err_index = index;
@@ -418,33 +506,26 @@ __device__ void finalize_step(const Dev& d, const Part& p, int status, int index
       c.err_dt = dt;
       c.err_h = err_h;
     }
-    c.bad_edge = kNone;
-    c.bad_cell = kNone;
     c.bad_speed = kNone;
     c.active = 0;
-    *d.ctl = c;
-    if (use_cond) cudaGraphSetConditional(cond, 0);
-    return;
+    return 0;
   }
   // commit (engine.hpp:300-307)
-  const double max_speed_pre = c.max_speed;
-  c.clipped += p.clip;
-  c.events += p.events;
+  ci.max_speed_pre = c.max_speed;
   c.cur ^= 1;
   c.t = last ? sp.t_end : c.t + dt;
   c.step += 1;
-  const long long slot = sp.ring ? (c.n_rec % sp.rec_cap) : c.n_rec;
-  if (slot < sp.rec_cap) {
-    swe_step_record r;
-    r.step = c.step;
-    r.t = c.t;
-    r.dt = dt;
-    r.max_speed = max_speed_pre;
-    r.mass = p.mass;
-    d.rec[slot] = r;
-  }
+  ci.slot = sp.ring ? (c.n_rec % sp.rec_cap) : c.n_rec;
+  ci.step = c.step;
+  ci.t = c.t;
+  ci.dt = dt;
   c.n_rec += 1;
-  set_cfl_cache(&c, p, d.P);
+  // set_cfl_cache without the mass (engine.hpp:214)
+  c.dts = isfinite(lo) ? P.cfl * lo : P.dt_max;
+  c.max_speed = hi;
+  c.cfl_bad = c.bad_speed;
+  c.bad_speed = kNone;
+  c.cfl_valid = 1;
   // continue? (engine.hpp:355-358, :374-375)
   int go = c.t < sp.t_end && c.step < sp.max_steps && !(c.t >= sp.next_snap - 1e-12) &&
            (sp.ring || c.n_rec < sp.rec_cap);
@@ -454,7 +535,41 @@ __device__ void finalize_step(const Dev& d, const Part& p, int status, int index
     go = 0;
   }
   c.active = go;
-  *d.ctl = c;
+  return go;
+}
+
+__device__ __forceinline__ void commit_tail(Ctl& c, const StepParams& sp, const Part& p,
+                                            const CommitInfo& ci, swe_step_record* rec) {
+  if (!ci.ok) return;
+  c.clipped += p.clip;
+  c.events += p.events;
+  c.mass = p.mass;
+  if (ci.slot < sp.rec_cap) {
+    swe_step_record r;
+    r.step = ci.step;
+    r.t = ci.t;
+    r.dt = ci.dt;
+    r.max_speed = ci.max_speed_pre;
+    r.mass = p.mass;
+    rec[ci.slot] = r;
+  }
+}
+
+__device__ __forceinline__ int commit_core(Ctl& c, const StepParams& sp, const Part& p, int status,
+                                           int index, double err_h, const Phys& P,
+                                           swe_step_record* rec) {
+  CommitInfo ci;
+  const int go = commit_head(c, sp, p.lo, p.hi, status, index, err_h, P, ci);
+  commit_tail(c, sp, p, ci, rec);
+  return go;
+}
+
+__device__ void finalize_step(const Dev& d, const Part& p, int status, int index, double err_h,
+                              cudaGraphConditionalHandle cond, int use_cond) {
+  Ctl c = load_ctl(d.ctl);
+  const StepParams sp = *d.sp;
+  const int go = commit_core(c, sp, p, status, index, err_h, d.P, d.rec);
+  store_commit(d.ctl, c);
   if (use_cond) cudaGraphSetConditional(cond, go);
 }
 
@@ -505,9 +620,7 @@ __device__ void post_outcome(const Dev& d, const Part& p, int kind) {
   const unsigned long long tag = c.xseq + 1;
   x.tag = tag;
   __syncwarp();
-  if (lane == 0) {
-    d.ctl->bad_edge = kNone;
-    d.ctl->bad_cell = kNone;
+  if (lane == 0) {  // (bad_edge / bad_cell only fail a step: see store_commit)
     d.ctl->bad_speed = kNone;
     d.ctl->xseq = tag;
   }

@@ -780,8 +780,8 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_face, k_face_c, kBlock, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_cell, k_cell_c, kBlock, 0);
   x->tile_smem = d.stage ? tile_stage_smem_bytes(d.T, d.max_slots) : tile_smem_bytes(d.T, d.max_slots);
-  if (x->persistent)  // k_run's commit reduces the partials in the tile's shared memory
-    x->tile_smem = std::max(x->tile_smem, (size_t)kBlock * sizeof(Part));
+  if (x->persistent)  // k_run's control block keeps its scratch + Dev in the tile buffers
+    x->tile_smem = std::max(x->tile_smem, kRunCtlSmem);
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if ((long long)x->tile_smem + 1024 > smem_optin) {
@@ -815,16 +815,20 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
                                                     x->tile_threads, x->tile_smem);
       occ_run = L == 0 ? o : std::min(occ_run, o);
     }
-    if (occ_run < 1) x->persistent = false;
-    // cooperative launch: every CTA resident at once
-    x->grid_run = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_run)));
+    if (occ_run < 1 || sms * occ_run < 2) x->persistent = false;
+    // cooperative launch: every CTA resident at once -- W workers (as many
+    // as k_tile's grid, so both loops form the same partial sums) + 1 control
+    int W = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_run) - 1));
     if (const char* env = std::getenv("SWE_RUN_GRID"))  // test hook: fewer CTAs, more tiles each
-      x->grid_run = std::max(1, std::min(x->grid_run, std::atoi(env)));
+      W = std::max(1, std::min(W, std::atoi(env)));
+    x->grid_run = W + 1;
   }
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
   x->grid_tile = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_tile)));
-  d.part = x->alloc<Part>(std::max(std::max(x->grid_cell, x->grid_tile), x->grid_run));
+  if (x->persistent) x->grid_tile = std::min(x->grid_tile, x->grid_run - 1);  // same partials
+  // (two parities of the persistent kernel's worker partials)
+  d.part = x->alloc<Part>(2 * (size_t)std::max(std::max(x->grid_cell, x->grid_tile), x->grid_run));
   if (!d.part) return bail(SWE_CUDA);
 
   Ctl c0{};
@@ -1480,7 +1484,7 @@ int swe_dev_run_ranks(swe_dev_ctx* const* xs, int n, long long nsteps, double t_
         x->tile_threads != xs[0]->tile_threads || x->d.L.rank != r || x->d.L.nranks != n)
       return fail_invalid("swe_dev_run_ranks: contexts must be persistent, linked as ranks "
                           "0..n-1 of n, on one device");
-    G = std::min(G, std::min(x->d.ntiles, x->grid_run));
+    G = std::min(G, std::min(x->d.ntiles + 1, x->grid_run));  // workers + a control block
   }
   const int NT = xs[0]->tile_threads;
   size_t smem = 0;
@@ -1492,7 +1496,7 @@ int swe_dev_run_ranks(swe_dev_ctx* const* xs, int n, long long nsteps, double t_
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, xs[0]->device));
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kr, NT, smem));
   G = std::min(G, sms * occ / n);
-  if (G < 1) return fail_invalid("swe_dev_run_ranks: too many ranks for one device");
+  if (G < 2) return fail_invalid("swe_dev_run_ranks: too many ranks for one device");
   // CFL bound of the current state: every rank posts, then every rank waits
   // (phases, so no waiting kernel runs before all posts are done)
   std::vector<bool> posted(n, false);
@@ -1537,6 +1541,19 @@ int swe_dev_run_ranks(swe_dev_ctx* const* xs, int n, long long nsteps, double t_
     if (code != SWE_OK && worst == SWE_OK) worst = code;
   }
   return worst;
+}
+
+// experiment builds (SWE_RUN_TIMING=1): the persistent loop's phase-time
+// sums [work ns, epoch-wait ns, arrival-wait ns, commit ns, CTA-steps,
+// commits]; read and cleared
+int swe_dev_run_timing(swe_dev_ctx* x, long long* out, int n) {
+  if (!x || !out || !x->d.sync) return fail_invalid("swe_dev_run_timing: no persistent context");
+  Sync h;
+  CK(cudaStreamSynchronize(x->stream));
+  CK(cudaMemcpy(&h, x->d.sync, sizeof(Sync), cudaMemcpyDeviceToHost));
+  for (int i = 0; i < n && i < 12; ++i) out[i] = (long long)h.timing[i];
+  CK(cudaMemset(x->d.sync, 0, sizeof(Sync)));
+  return SWE_OK;
 }
 
 int swe_dev_last_record(swe_dev_ctx* x, swe_step_record* rec, swe_status* st) {

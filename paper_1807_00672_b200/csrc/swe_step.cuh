@@ -572,40 +572,248 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
 // ---------------------------------------------------------------------------
 constexpr int kRunDec = 128;  // skip decisions held per CTA (recomputed in chunks)
 
+// SWE_RUN_TIMING=1 (experiment builds): per-CTA globaltimer sums of the
+// persistent loop's phases in Sync::pad, read by swe_dev_run_timing
+#ifndef SWE_RUN_TIMING
+#define SWE_RUN_TIMING 0
+#endif
+#if SWE_RUN_TIMING
+#define RUN_T(k, v) atomicAdd(&sy->timing[k], (unsigned long long)(v))
+#else
+#define RUN_T(k, v) ((void)0)
+#endif
+
 __device__ __forceinline__ bool run_skip(const Dev& d, const int* fl, int t, int tag) {
-  if (__ldcg(fl + t) != tag) return false;
+  // three round trips, not one per neighbour: the own flag and the list
+  // bounds together, then up to 8 neighbour ids, then their flags
+  const int own = __ldcg(fl + t);
   const int v0 = __ldg(d.nbr_off + t), v1 = __ldg(d.nbr_off + t + 1);
+  if (own != tag) return false;
   bool ok = true;
-  for (int v = v0; v < v1; ++v) {
-    const int nb = __ldg(d.nbr + v);
-    ok = ok && nb < d.ntiles && __ldcg(fl + nb) == tag;
+  for (int v = v0; v < v1; v += 8) {
+    int nbv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) nbv[k] = v + k < v1 ? __ldg(d.nbr + v + k) : -1;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int q = nbv[k];
+      const int f = q < 0 ? tag : (q < d.ntiles ? __ldcg(fl + q) : 0);
+      ok &= f == tag;
+    }
   }
   // a tile whose cells peers hold as ghosts is computed (its pushes run there)
   if (d.L.nranks > 0 && __ldg(d.L.tile_push + t + 1) > __ldg(d.L.tile_push + t)) ok = false;
   return ok;
 }
 
-// the last CTA to arrive: reduce the step's partials in the fixed order and
-// commit it (k_finalize / k_exchange's code), then publish the epoch.  Kept
-// out of line: its control-block copies would otherwise cost the step loop
-// registers (ptxas spills).
+// The control CTA of the persistent kernel (the grid's last block; it owns no
+// tiles): per step it waits for every worker's arrival, reduces their
+// partials in the fixed order and commits the step -- k_finalize /
+// k_exchange's code, so the same bits -- then publishes it as the next epoch.
+// The workers meanwhile start the next step's fluxes.  Its Dev lives in its
+// shared memory (the tile buffers are free), off the L1 the per-step acquire
+// invalidates; kept out of line so it costs the workers no registers.
+constexpr size_t kRunCtlOff = (sizeof(Part) * kBlock + 63) / 64 * 64;  // Dev, Ctl, StepParams
+constexpr size_t kRunCtlSmem =
+    kRunCtlOff + (sizeof(Dev) + 63) / 64 * 64 + (sizeof(Ctl) + 63) / 64 * 64 + sizeof(StepParams);
+
 template <bool LINK>
-__device__ __noinline__ void run_commit(const Dev* dg, Sync* sy, int nb, unsigned epoch,
-                                        Part* scratch) {
-  const Dev& d = *dg;  // the context's Dev in global memory (no local copy of the parameter)
-  const Part p = reduce_parts_into(d.part, nb, scratch);  // tile smem is free here
-  if (LINK) {
-    if (threadIdx.x < 32) {
-      post_outcome(d, p, 0);
-      wait_and_commit(d, 0, cudaGraphConditionalHandle{}, 0);
-    }
-  } else if (threadIdx.x == 0) {
-    finalize_local(d, p, cudaGraphConditionalHandle{}, 0);
+__device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
+  extern __shared__ double smem[];
+  // the tile buffers of this block hold: partial scratch, its Dev, the
+  // authoritative control block during the launch, the step parameters
+  char* base = reinterpret_cast<char*>(smem);
+  Part* scratch = reinterpret_cast<Part*>(base);
+  Dev* ds = reinterpret_cast<Dev*>(base + kRunCtlOff);
+  Ctl& s_c = *reinterpret_cast<Ctl*>(base + kRunCtlOff + (sizeof(Dev) + 63) / 64 * 64);
+  StepParams& s_sp = *reinterpret_cast<StepParams*>(base + kRunCtlOff + (sizeof(Dev) + 63) / 64 * 64 +
+                                                    (sizeof(Ctl) + 63) / 64 * 64);
+  __shared__ int s_go;
+  __shared__ CommitInfo s_ci;
+  {
+    const unsigned* src = reinterpret_cast<const unsigned*>(dg);
+    unsigned* dst = reinterpret_cast<unsigned*>(ds);
+    for (int i = threadIdx.x; i < (int)(sizeof(Dev) / 4); i += blockDim.x) dst[i] = __ldg(src + i);
   }
   __syncthreads();
+  const Dev& d = *ds;
   if (threadIdx.x == 0) {
-    __threadfence();
-    st_release_gpu(&sy->epoch, epoch);
+    s_c = load_ctl(d.ctl);  // as the gate left it
+    s_sp = *d.sp;
+    s_go = s_c.active;
+  }
+  __syncthreads();
+  if (!s_go) return;  // the gate closed the loop: no worker runs a step
+  for (unsigned it = 0;; ++it) {
+    const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
+    const int par = (int)(s_c.step & 1);
+    const Part* parts = d.part + (size_t)par * nb;
+    if (LINK) {  // the exchange carries every sum: reduce first, then post / wait / commit
+      if (threadIdx.x == 0) {
+        poll_until(&sy->arrive, (unsigned)nb * (it + 1));
+        fence_acq_rel_gpu();
+      }
+      __syncthreads();
+      const Part p = reduce_parts_into(parts, nb, scratch);
+      if (threadIdx.x < 32) {
+        post_outcome(d, p, 0);
+        wait_and_commit(d, 0, cudaGraphConditionalHandle{}, 0);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        s_c.step = __ldcg(&d.ctl->step);
+        s_go = __ldcg(&d.ctl->active);
+        __threadfence();
+        st_release_gpu(&sy->epoch, it + 1);
+      }
+      __syncthreads();
+      if (!s_go) return;
+      continue;
+    }
+    if (threadIdx.x == 0) {
+      poll_until(&sy->arrive, (unsigned)nb * (it + 1));
+      fence_acq_rel_gpu();  // every worker's partials, error slots and state
+      const unsigned long long c0 = SWE_RUN_TIMING ? global_ns() : 0;
+      const double lo = __longlong_as_double((long long)__ldcg(&sy->lo[par]));
+      const double hi = __longlong_as_double((long long)__ldcg(&sy->hi[par]));
+      const int bad_edge = __ldcg(&d.ctl->bad_edge), bad_cell = __ldcg(&d.ctl->bad_cell);
+      const int bad_speed = __ldcg(&d.ctl->bad_speed);
+      sy->lo[par] = 0x7ff0000000000000ULL;  // this parity's next use: two steps on
+      sy->hi[par] = 0ULL;
+      int status = SWE_OK, index = kNone;  // finalize_local (engine.hpp:168-169, :292-297)
+      double err_h = 0.0;
+      if (bad_edge != kNone) {
+        status = SWE_NEGATIVE_DEPTH;
+        index = bad_edge;
+      } else if (bad_cell != kNone) {
+        status = SWE_BLOWUP;
+        index = bad_cell;
+        err_h = d.h[s_c.cur ^ 1][d.c_new[bad_cell]];
+      }
+      Ctl c = s_c;
+      c.bad_speed = bad_speed;
+      CommitInfo ci;
+      s_go = commit_head(c, s_sp, lo, hi, status, index, err_h, d.P, ci);
+      store_commit(d.ctl, c);
+      s_c = c;
+      s_ci = ci;
+      __threadfence();
+      st_release_gpu(&sy->epoch, it + 1);  // the workers update the next step now
+      RUN_T(3, global_ns() - c0);
+      RUN_T(5, 1);
+      RUN_T(2, c0 - w0);
+    }
+    __syncthreads();
+    // off the critical path: the step's sums in the fixed order (the same
+    // bits as k_finalize), the clip ledger and the record
+    const unsigned long long r0 = SWE_RUN_TIMING ? global_ns() : 0;
+    const Part p = reduce_parts_into(parts, nb, scratch);
+    if (threadIdx.x == 0) {
+      Ctl c = s_c;
+      commit_tail(c, s_sp, p, s_ci, d.rec);
+      d.ctl->clipped = c.clipped;
+      d.ctl->events = c.events;
+      d.ctl->mass = c.mass;
+      s_c = c;
+      RUN_T(7, global_ns() - r0);
+    }
+    __syncthreads();
+    if (!s_go) return;
+  }
+}
+
+// staging + edge evaluation of one computed tile of the persistent kernel
+// (k_tile's code).  CG: the state is read through L2 (ld.global.cg) -- the
+// first tile of a step runs before the CTA's acquire of the new epoch, and L1
+// may still hold lines of this buffer from two steps ago.
+#ifndef SWE_RUN_NC
+#define SWE_RUN_NC 0  // experiment only: .nc loads of the state (not valid across steps)
+#endif
+template <bool CG>
+__device__ __forceinline__ double ld_state(const double* p) {
+  if (CG) return __ldcg(p);
+#if SWE_RUN_NC
+  return __ldg(p);
+#else
+  return *p;
+#endif
+}
+
+template <int NT, bool CG>
+__device__ __forceinline__ void run_tile_edges(const Dev& d, const double* H, const double* QX,
+                                               const double* QY, int t, int c0, int nc,
+                                               double* sh, double* sq, double* sr, double* sz,
+                                               double* tm, double* tx, double* ty) {
+  Ctl* ctl = d.ctl;
+  const Phys P = d.P;
+  for (int i = threadIdx.x; i < nc; i += NT) {
+    sh[i] = ld_state<CG>(H + c0 + i);
+    sq[i] = ld_state<CG>(QX + c0 + i);
+    sr[i] = ld_state<CG>(QY + c0 + i);
+    sz[i] = ldg_geo(d.cg + c0 + i).z;
+  }
+  const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
+  const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
+  __syncthreads();
+  for (int jj = threadIdx.x; jj < ns; jj += NT) {
+    const int e = jj < no ? e0 + jj : __ldg(d.halo + h0 + (jj - no));
+    const int2 ek = __ldg(d.ek + e);
+    const double2 nn = __ldg(d.enxy + e);
+    const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
+    const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
+    const bool w = ek.y == -1;
+    const int il = cl - c0, ir = (w ? cl : cr) - c0;
+    const bool inL = (unsigned)il < (unsigned)nc;
+    Cons uL, uR;
+    double zl, zr;
+    if (inL) {
+      uL = Cons{sh[il], sq[il], sr[il]};
+      zl = sz[il];
+    } else {
+      uL = Cons{ld_state<CG>(H + cl), ld_state<CG>(QX + cl), ld_state<CG>(QY + cl)};
+      zl = __ldg(d.z + cl);
+    }
+    if ((unsigned)ir < (unsigned)nc) {
+      uR = Cons{sh[ir], sq[ir], sr[ir]};
+      zr = sz[ir];
+    } else {
+      const int c = ir + c0;
+      uR = Cons{ld_state<CG>(H + c), ld_state<CG>(QX + c), ld_state<CG>(QY + c)};
+      zr = __ldg(d.z + c);
+    }
+    if (uL.h < 0.0 || (!w && uR.h < 0.0)) {  // engine.hpp:147-153
+      atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
+      continue;
+    }
+    const double hg = 0.5 * P.g;
+    const int sl = 3 * il + (int)((unsigned)ek.x >> 30);
+    if (!w) {
+      double f0, lx, ly, rx, ry;
+      interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
+      const int2 ek2 = __ldg(d.ek + e);
+      const double len2 = __ldg(d.len + e);
+      const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
+      if ((unsigned)il2 < (unsigned)nc) {
+        const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
+        const double ownL = (hg * uL.h) * uL.h;
+        tm[s2] = f0 * len2;
+        tx[s2] = (lx - ownL * nx) * len2;
+        ty[s2] = (ly - ownL * ny) * len2;
+      }
+      if ((unsigned)ir2 < (unsigned)nc) {
+        const int s3 = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
+        const double ownR = (hg * uR.h) * uR.h;
+        tm[s3] = (-f0) * len2;
+        tx[s3] = (rx - ownR * (-nx)) * len2;
+        ty[s3] = (ry - ownR * (-ny)) * len2;
+      }
+    } else if (inL) {
+      const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
+      const double ownL = (hg * uL.h) * uL.h;
+      tm[sl] = f.m * len;
+      tx[sl] = (f.fx - ownL * nx) * len;
+      ty[sl] = (f.fy - ownL * ny) * len;
+    }
   }
 }
 
@@ -624,7 +832,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
   double* ty = tx + 3 * T;
   const Phys P = d.P;
   __shared__ unsigned char s_dec[kRunDec];
-  __shared__ int s_cur, s_active, s_last;
+  __shared__ int s_cur, s_active;
   __shared__ long long s_step;
   __shared__ double s_dt;
 
@@ -632,8 +840,12 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
   // finalizing CTA (epoch >= it), read by thread 0 after the acquire
   auto read_view = [&](unsigned it) {
     if (threadIdx.x == 0) {
-      if (it > 0)
-        while (ld_acquire_gpu(&sy->epoch) < it) __nanosleep(20);
+      if (it > 0) {  // relaxed polls (an acquire per poll would flush L1 each time)
+        const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
+        poll_until(&sy->epoch, it);
+        fence_acq_rel_gpu();  // acquire the commit (and the peers' halo pushes)
+        RUN_T(1, global_ns() - w0);
+      }
       s_cur = __ldcg(&ctl->cur);
       s_step = __ldcg(&ctl->step);
       s_active = __ldcg(&ctl->active);
@@ -649,6 +861,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
   double dt = s_dt;
   const int ntl = bid < d.ntiles ? (d.ntiles - bid + nb - 1) / nb : 0;  // this CTA's tiles
 
+  unsigned long long t_step = SWE_RUN_TIMING ? global_ns() : 0;
   for (unsigned it = 0;; ++it) {
     const int tag = (int)(step + 1);
     const int* fl = d.pflag + (size_t)(step & 1) * d.ntiles;       // flags of this state
@@ -661,6 +874,14 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
     double* NQY = d.qy[cur ^ 1];
     CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
     bool viewed = it == 0;  // dt / stop of this step known
+#ifndef SWE_RUN_OVERLAP
+#define SWE_RUN_OVERLAP 1  // 0 (experiment): wait for the commit before the first tile
+#endif
+    if (!SWE_RUN_OVERLAP && !viewed) {
+      if (!read_view(it)) return;
+      viewed = true;
+      dt = s_dt;
+    }
     for (int j = 0; j < ntl;) {
       if (j % kRunDec == 0) {  // skip decisions of the next chunk of tiles
         __syncthreads();
@@ -705,75 +926,10 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
         viewed = true;
         dt = s_dt;
       }
-      for (int i = threadIdx.x; i < nc; i += NT) {
-        sh[i] = H[c0 + i];
-        sq[i] = QX[c0 + i];
-        sr[i] = QY[c0 + i];
-        sz[i] = ldg_geo(d.cg + c0 + i).z;
-      }
-      const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
-      const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
-      __syncthreads();
-      for (int jj = threadIdx.x; jj < ns; jj += NT) {
-        const int e = jj < no ? e0 + jj : __ldg(d.halo + h0 + (jj - no));
-        const int2 ek = __ldg(d.ek + e);
-        const double2 nn = __ldg(d.enxy + e);
-        const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
-        const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
-        const bool w = ek.y == -1;
-        const int il = cl - c0, ir = (w ? cl : cr) - c0;
-        const bool inL = (unsigned)il < (unsigned)nc;
-        Cons uL, uR;
-        double zl, zr;
-        if (inL) {
-          uL = Cons{sh[il], sq[il], sr[il]};
-          zl = sz[il];
-        } else {
-          uL = Cons{H[cl], QX[cl], QY[cl]};
-          zl = __ldg(d.z + cl);
-        }
-        if ((unsigned)ir < (unsigned)nc) {
-          uR = Cons{sh[ir], sq[ir], sr[ir]};
-          zr = sz[ir];
-        } else {
-          const int c = ir + c0;
-          uR = Cons{H[c], QX[c], QY[c]};
-          zr = __ldg(d.z + c);
-        }
-        if (uL.h < 0.0 || (!w && uR.h < 0.0)) {  // engine.hpp:147-153
-          atomicMin(&ctl->bad_edge, __ldg(d.e_orig + e));
-          continue;
-        }
-        const double hg = 0.5 * P.g;
-        const int sl = 3 * il + (int)((unsigned)ek.x >> 30);
-        if (!w) {
-          double f0, lx, ly, rx, ry;
-          interior_edge(uL, zl, uR, zr, nx, ny, P, f0, lx, ly, rx, ry);
-          const int2 ek2 = __ldg(d.ek + e);
-          const double len2 = __ldg(d.len + e);
-          const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
-          if ((unsigned)il2 < (unsigned)nc) {
-            const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
-            const double ownL = (hg * uL.h) * uL.h;
-            tm[s2] = f0 * len2;
-            tx[s2] = (lx - ownL * nx) * len2;
-            ty[s2] = (ly - ownL * ny) * len2;
-          }
-          if ((unsigned)ir2 < (unsigned)nc) {
-            const int s3 = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
-            const double ownR = (hg * uR.h) * uR.h;
-            tm[s3] = (-f0) * len2;
-            tx[s3] = (rx - ownR * (-nx)) * len2;
-            ty[s3] = (ry - ownR * (-ny)) * len2;
-          }
-        } else if (inL) {
-          const Flux f = wall(uL, nx, ny, P);  // engine.hpp:155-159
-          const double ownL = (hg * uL.h) * uL.h;
-          tm[sl] = f.m * len;
-          tx[sl] = (f.fx - ownL * nx) * len;
-          ty[sl] = (f.fy - ownL * ny) * len;
-        }
-      }
+      if (viewed)
+        run_tile_edges<NT, false>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
+      else  // before the epoch: L1 may hold this buffer from two steps ago
+        run_tile_edges<NT, true>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
       __syncthreads();
       if (!viewed) {  // the first computed tile's edges are done: now dt / stop
         if (!read_view(it)) return;
@@ -823,20 +979,33 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
       if (!read_view(it)) return;
       viewed = true;
     }
-    block_reduce_part(a.lo, a.hi, a.mass, a.clip, a.ev, d.part + bid);
-    // arrive; the last CTA commits the step (k_finalize / k_exchange's code)
-    __syncthreads();
+    const int par = (int)(step & 1);
+    const Part bp = block_reduce_part_ret(a.lo, a.hi, a.mass, a.clip, a.ev,
+                                          d.part + (size_t)par * nb + bid);
+    // fold the CFL bound / max speed in (exact, order-independent), then
+    // arrive (a release: this CTA's state, flags and partials are in L2)
     if (threadIdx.x == 0) {
-      __threadfence();
-      const unsigned old = atomicAdd(&sy->arrive, 1u);
-      s_last = old + 1 == (unsigned)nb * (it + 1);
-      if (s_last) __threadfence();
+      if (SWE_RUN_TIMING) {
+        RUN_T(0, global_ns() - t_step);
+        RUN_T(4, 1);
+      }
+      if (!LINK) {
+        atomicMin(&sy->lo[par], (unsigned long long)__double_as_longlong(bp.lo));
+        atomicMax(&sy->hi[par], (unsigned long long)__double_as_longlong(bp.hi));
+      }
+      atom_add_release_gpu(&sy->arrive, 1u);
     }
-    __syncthreads();
-    if (s_last) run_commit<LINK>(dg, sy, nb, it + 1, reinterpret_cast<Part*>(smem));
-    // every CTA has arrived: the next state and its dry-tile flags are complete
-    if (threadIdx.x == 0)
-      while (ld_acquire_gpu(&sy->arrive) < (unsigned)nb * (it + 1)) __nanosleep(20);
+    // every worker has arrived: the next state and its dry-tile flags are
+    // complete.  Relaxed polls: the CTA reads them through L2 (ld.cg) until
+    // its acquire of the epoch, which flushes L1 once per step
+    if (threadIdx.x == 0) {
+      const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
+      poll_until(&sy->arrive, (unsigned)nb * (it + 1));
+      if (SWE_RUN_TIMING) {
+        t_step = global_ns();
+        RUN_T(6, t_step - w0);
+      }
+    }
     __syncthreads();
     cur ^= 1;  // the next step, provisionally (confirmed by its epoch)
     step += 1;
@@ -845,7 +1014,9 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
 
 template <int NT, bool LINK>
 __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d, const Dev* dg) {
-  run_body<NT, LINK>(d, dg, d.sync, blockIdx.x, gridDim.x);
+  const int nb = gridDim.x - 1;  // workers; the last block controls
+  if ((int)blockIdx.x == nb) run_control<LINK>(dg, d.sync, nb);
+  else run_body<NT, LINK>(d, dg, d.sync, blockIdx.x, nb);
 }
 
 // P linked ranks' persistent kernels as ONE cooperative launch on one device
@@ -855,7 +1026,9 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d, const De
 template <int NT>
 __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run_ranks(const Dev* devs, int G) {
   const Dev& d = devs[blockIdx.x / G];
-  run_body<NT, true>(d, &d, d.sync, blockIdx.x % G, G);
+  const int b = blockIdx.x % G, nb = G - 1;  // G - 1 workers and a control block per rank
+  if (b == nb) run_control<true>(&d, d.sync, nb);
+  else run_body<NT, true>(d, &d, d.sync, b, nb);
 }
 
 // ---------------------------------------------------------------------------

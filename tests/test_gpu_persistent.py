@@ -58,13 +58,13 @@ def test_persistent_equals_graph_loop(name, scale):
 
 
 def test_persistent_matches_oracle_with_many_tiles_per_cta(coracle):
-    """Two CTAs: every CTA walks hundreds of tiles, so its skip decisions are
+    """Two worker CTAs: every one walks hundreds of tiles, so its skip decisions are
     formed in several chunks (kRunDec) per step."""
     sc = api.make_scenario("sloping_wet_dry", scale=0.05)
     m = api.build_mesh(sc.raw, sc.bed, sc.manning)
     s = solver(m, SWE_RUN_GRID=2)
     info = s.info()
-    assert info["grid_run"] == 2 and info["tiles"] > 2 * 128
+    assert info["grid_run"] == 3 and info["tiles"] > 2 * 128  # 2 workers + the control block
     s.set_state(sc.state)
     recs = s.advance(1e30, max_steps=200)
     got, _, _ = s.get_state()
@@ -128,7 +128,7 @@ def test_linked_ranks_run_concurrently_in_one_launch(P):
 
 def test_linked_ranks_one_cta_each_many_tiles():
     sc, m, parts = _linked(2, scale=0.05)
-    recs = dist.run_ranks(parts, 60, grid=1)
+    recs = dist.run_ranks(parts, 60, grid=2)  # one worker + the control block per rank
     got = api.FieldState.zeros(m.n_cells)
     for p in parts:
         p.gather_owned(got)
