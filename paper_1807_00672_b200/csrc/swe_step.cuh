@@ -697,8 +697,7 @@ __device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
       store_commit(d.ctl, c);
       s_c = c;
       s_ci = ci;
-      __threadfence();
-      st_release_gpu(&sy->epoch, it + 1);  // the workers update the next step now
+      st_release_gpu(&sy->epoch, it + 1);  // (a release: orders the stores above)
       RUN_T(3, global_ns() - c0);
       RUN_T(5, 1);
       RUN_T(2, c0 - w0);
