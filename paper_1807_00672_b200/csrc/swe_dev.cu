@@ -59,6 +59,8 @@ size_t arena_offset(long long C, int k) {
   return box + (size_t)k * arr;
 }
 
+constexpr int kPersistentMaxCells = 600000;
+
 int fail_invalid(const char* msg) {
   g_last_error = msg;
   return SWE_INVALID;
@@ -623,7 +625,11 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_GRAPH_UNROLL")) x->graph_unroll = std::max(1, std::atoi(env));
-  x->persistent = true;  // SWE_PERSISTENT=0: the CUDA-graph loop of k_tile + k_finalize
+  // run loop: the persistent kernel where a step's fixed cost matters (small
+  // meshes: 10k cells 7.9 vs 11.4 us per step), the CUDA graph of k_tile +
+  // k_finalize above (on par from ~1M cells on: 1M 31.7 vs 31.5 us, 10M
+  // 472 vs 470 us).  SWE_PERSISTENT=0/1 forces either.
+  x->persistent = d.C_own <= kPersistentMaxCells;
   if (const char* env = std::getenv("SWE_PERSISTENT")) x->persistent = std::atoi(env) != 0;
   d.skip = 1;  // dry-tile skipping (fused kernel); SWE_NO_DRY_SKIP=1 turns it off
   if (const char* env = std::getenv("SWE_NO_DRY_SKIP")) d.skip = std::atoi(env) == 0;
@@ -825,8 +831,10 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   }
   x->grid_face = std::max(1, std::min(blocks_for(E), sms * std::max(1, occ_face)));
   x->grid_cell = std::max(1, std::min(blocks_for(C), sms * std::max(1, occ_cell)));
-  x->grid_tile = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_tile)));
-  if (x->persistent) x->grid_tile = std::min(x->grid_tile, x->grid_run - 1);  // same partials
+  // one resident CTA short of a full wave: the persistent kernel's control
+  // block takes that slot, so both run loops form the same partial sums
+  x->grid_tile = std::max(1, std::min(d.ntiles, sms * std::max(1, occ_tile) - 1));
+  if (x->persistent) x->grid_tile = std::min(x->grid_tile, x->grid_run - 1);
   // (two parities of the persistent kernel's worker partials)
   d.part = x->alloc<Part>(2 * (size_t)std::max(std::max(x->grid_cell, x->grid_tile), x->grid_run));
   if (!d.part) return bail(SWE_CUDA);
@@ -1873,7 +1881,10 @@ int swe_dev_cell_skip(swe_dev_ctx* x, unsigned char* skipped) {
   if (int rc = sync_ctl(x)) return rc;
   unsigned char* dv = nullptr;
   CK(cudaMalloc(&dv, (size_t)C));
-  if (x->d.skip) {
+  if (x->d.skip && x->persistent) {
+    k_cell_skip_run<<<blocks_for(C), kBlock, 0, x->stream>>>(x->d, x->h_ctl->step, dv);
+    ++g_launches;
+  } else if (x->d.skip) {
     k_cell_skip<<<blocks_for(C), kBlock, 0, x->stream>>>(x->d, (int)(x->h_ctl->step + 1), dv);
     ++g_launches;
   } else {

@@ -1011,6 +1011,14 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
   }
 }
 
+// swe_dev_cell_skip of a persistent context: the decisions k_run makes next
+__global__ void k_cell_skip_run(Dev d, long long step, unsigned char* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= d.C) return;
+  const int* fl = d.pflag + (size_t)(step & 1) * d.ntiles;
+  out[d.c_orig[c]] = (c < d.C_own && run_skip(d, fl, c / d.T, (int)(step + 1))) ? 1 : 0;
+}
+
 template <int NT, bool LINK>
 __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_run(Dev d, const Dev* dg) {
   const int nb = gridDim.x - 1;  // workers; the last block controls

@@ -154,3 +154,39 @@ def test_linked_ranks_error_stops_every_rank():
         p.set_state(st)
     with pytest.raises(api.NumericError, match=f"non-finite velocity in cell {bad}$"):
         dist.run_ranks(parts, 5)
+
+
+def test_cell_skip_pattern_matches_the_graph_loop():
+    """swe_dev_cell_skip (the cost pattern behind measured_cost_weights) reads
+    the persistent kernel's own dry-tile flags."""
+    sc = api.make_scenario("sloping_wet_dry", scale=0.05)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    a, b = solver(m), solver(m, SWE_PERSISTENT=0)
+    pats = []
+    for s in (a, b):
+        s.set_state(sc.state)
+        s.advance(1e30, max_steps=30)
+        pats.append(s.cell_skip())
+    assert pats[0].sum() > 0 and np.array_equal(pats[0], pats[1])
+
+
+@pytest.mark.parametrize("name", ["three_mounds_friction", "channel"])
+def test_persistent_full_size_equals_graph_loop(name):
+    """Above kPersistentMaxCells the graph loop is the default; forced
+    persistent at full size (1.06M / 10.26M cells, 1183 workers, many tiles
+    per worker) is the same computation bit for bit."""
+    sc = api.make_scenario(name)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    a, b = solver(m, SWE_PERSISTENT=1), solver(m)
+    assert a.info()["persistent"] == 1 and b.info()["persistent"] == 0
+    out = []
+    for s in (a, b):
+        s.set_state(sc.state)
+        recs = np.concatenate([s.advance(1e30, max_steps=k) for k in (3, 60)])
+        st, t, step = s.get_state()
+        out.append((st, recs, s.ledger()))
+        s.close()
+    (sa, ra, la), (sb, rb, lb) = out
+    assert bit_equal(ra, rb) and la == lb
+    for k in ("h", "qx", "qy"):
+        assert bit_equal(getattr(sa, k), getattr(sb, k)), k

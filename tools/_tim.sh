@@ -1,2 +1,4 @@
-timeout 300 python -m pytest tests/test_gpu_persistent.py -q -x --timeout 120 > gpurun_out/r02_persist_a.log 2>&1; echo rc=$? >> gpurun_out/r02_persist_a.log
-timeout 1500 tools/ab_persist.sh
+for c in "channel --scale 0.3536" "channel --scale 0.5" "three_mounds_friction"; do
+  echo "tim $(SWE_B200_LIB=exp/tim/libswe_b200.so timeout 300 python tools/run_timing.py --config $c 2>&1 | tail -1)"
+  echo "graph $(SWE_PERSISTENT=0 timeout 300 python tools/run_timing.py --config $c 2>&1 | tail -1)"
+done > gpurun_out/r02_run_timing.txt
