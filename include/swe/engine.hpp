@@ -34,19 +34,46 @@
 
 namespace swe {
 
+/// The caller's process group for one-process-per-GPU runs (MPI,
+/// torch.distributed, threads): rank / size and an allgather of byte blobs
+/// (every rank's blob, in rank order).  barrier is optional (lockstep
+/// debugging of ranks that share a device).
+struct Comm {
+  int rank = 0;
+  int size = 1;
+  std::function<std::vector<std::string>(const std::string&)> allgather;
+  std::function<void()> barrier;
+};
+
 /// Reference plugin point (engine.hpp:24-31).  The B200 engine always runs
 /// on the device; `device` selects the CUDA ordinal.  kind/threads are
 /// accepted for source compatibility and do not change results (the
-/// reference's backends are bitwise identical too).
+/// reference's backends are bitwise identical too).  Multi-GPU
+/// (swe/multigpu.hpp): gpus > 1 drives that many devices from this process
+/// (devices lists them; default device, device+1, ...), or comm makes this
+/// process one rank of a one-process-per-GPU run.  lockstep steps the parts
+/// phase by phase (parts sharing one device; debugging).
 struct BackendSpec {
   enum class Kind { sequential, parallel };
   Kind kind = Kind::sequential;
   int threads = 1;
   bool deterministic = true;
   int device = 0;
+  int gpus = 1;
+  std::vector<int> devices;
+  const Comm* comm = nullptr;
+  bool lockstep = false;
 
   bool is_parallel() const { return kind == Kind::parallel && threads > 1; }
 };
+
+struct Simulation;
+struct RunStats;
+struct RunOptions;
+namespace detail {
+inline RunStats run_multi(Simulation& sim, const Mesh& mesh, const PhysParams& p,
+                   const BackendSpec& backend, const RunOptions& opt);
+}  // namespace detail
 
 struct FieldState {
   std::vector<double> h, qx, qy;
@@ -451,6 +478,7 @@ inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
                     const BackendSpec& backend, const RunOptions& opt) {
   using clock = std::chrono::steady_clock;
   if (!(opt.t_end > 0.0)) throw config_error("run: t_end must be > 0");
+  if (backend.gpus > 1 || backend.comm) return detail::run_multi(sim, mesh, p, backend, opt);
   const auto hold = detail::device_mesh(mesh, p, backend.device);
   auto& dm = *hold;
   swe_dev_ctx* ctx = dm.ctx();
@@ -590,3 +618,5 @@ inline RunStats run(Simulation& sim, const Mesh& mesh, const PhysParams& p,
 }
 
 }  // namespace swe
+
+#include "swe/multigpu.hpp"  // run()'s multi-GPU path (backend.gpus / backend.comm)

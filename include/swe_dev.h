@@ -208,7 +208,8 @@ SWE_API int swe_dev_link_export(swe_dev_ctx* ctx, void** arena, unsigned char* i
 /* Link the context as `rank` of `nranks`.  Peers' arenas come either as
  * pointers valid in this process (arenas[q], contexts of this process, same
  * or peer-enabled devices) or as IPC handles (ipc_handles[64*q], other
- * processes).  peer_cells[q] = n_cells of rank q.  Push entry j sends owned
+ * processes; a NULL arenas[q] falls back to ipc_handles for that rank).
+ * peer_cells[q] = n_cells of rank q.  Push entry j sends owned
  * cell push_cell[j] (reference-local id) to ghost push_ghost[j] (local id on
  * rank push_rank[j]).  gcell[C] / gedge[E]: local -> global ids (NULL =
  * identity). */

@@ -74,6 +74,19 @@ def build_api_driver(verbose: bool = False, force: bool = False) -> Path:
     return out
 
 
+def build_multigpu_driver(verbose: bool = False, force: bool = False) -> Path:
+    """tests/cpp/multigpu_driver.cpp: the multi-GPU path of the drop-in API
+    (include/swe/multigpu.hpp) driven as a reference caller would."""
+    src = ROOT / "tests" / "cpp" / "multigpu_driver.cpp"
+    out = ROOT / "tests" / "cpp" / "multigpu_driver"
+    headers = list((INC / "swe").glob("*.hpp")) + list(INC.glob("*.h"))
+    if force or _stale(out, [src, LIB, *headers]):
+        _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", f"-I{INC}", src, "-o", out,
+              f"-L{PKG}", "-lswe_b200", "-pthread",
+              "-Wl,-rpath,$ORIGIN/../../paper_1807_00672_b200"], verbose)
+    return out
+
+
 JSON_INC = Path("/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/"
                 "thirdparty/nlohmann")
 REF_INC = Path("/root/reference/proj/include")
@@ -159,6 +172,7 @@ def build_oracle(verbose: bool = False) -> None:
 def build_all(verbose: bool = False, force: bool = False) -> None:
     build_library(verbose, force)
     build_api_driver(verbose, force)
+    build_multigpu_driver(verbose, force)
     build_harness_driver(verbose, force)
     build_oracle(verbose)
     build_reference_tests(verbose, force)

@@ -1336,7 +1336,7 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
   for (int q = 0; q < nranks; ++q) {
     if (q == rank) {
       base[q] = x->arena;
-    } else if (arenas) {
+    } else if (arenas && arenas[q]) {  // a context of this process
       base[q] = (char*)arenas[q];
       cudaPointerAttributes a{};
       CK(cudaPointerGetAttributes(&a, base[q]));
