@@ -165,6 +165,22 @@ def build_reference_tests(verbose: bool = False, force: bool = False) -> None:
                           [REF_INC], [], verbose, force, extra=["-fopenmp"])
 
 
+def build_io_ext_driver(verbose: bool = False, force: bool = False) -> Path:
+    """tests/cpp/io_ext_driver.cpp: the parallel VTK writer and backend.gpus
+    next to the reference's io.hpp (needs /root/reference + json.hpp; the
+    binary travels prebuilt)."""
+    src = ROOT / "tests" / "cpp" / "io_ext_driver.cpp"
+    out = ROOT / "tests" / "cpp" / "io_ext_driver"
+    if not (REF_INC.exists() and (JSON_INC / "json.hpp").exists()):
+        return out
+    headers = list((INC / "swe").glob("*.hpp")) + list(INC.glob("*.h"))
+    if force or _stale(out, [src, LIB, *headers]):
+        _run(["g++", "-O2", "-std=c++20", "-ffp-contract=off", f"-I{INC}", f"-I{REF_INC}",
+              f"-I{JSON_INC}", src, "-o", out, f"-L{PKG}", "-lswe_b200", "-pthread",
+              "-Wl,-rpath,$ORIGIN/../../paper_1807_00672_b200"], verbose)
+    return out
+
+
 def build_oracle(verbose: bool = False) -> None:
     _run(["make", "-s", "-C", ROOT / "oracle"], verbose)
 
@@ -174,6 +190,7 @@ def build_all(verbose: bool = False, force: bool = False) -> None:
     build_api_driver(verbose, force)
     build_multigpu_driver(verbose, force)
     build_harness_driver(verbose, force)
+    build_io_ext_driver(verbose, force)
     build_oracle(verbose)
     build_reference_tests(verbose, force)
 
