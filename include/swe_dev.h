@@ -258,6 +258,10 @@ SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
  * partitions, paper_1807_00672_b200/dist.py measured_cost_weights). */
 SWE_API int swe_dev_cell_skip(swe_dev_ctx* ctx, unsigned char* skipped);
 
+/* The device cell order: order[i] = reference cell stored at device position
+ * i (the blocked-Hilbert renumbering; ghosts of a part keep their place). */
+SWE_API int swe_dev_cell_order(swe_dev_ctx* ctx, int* order);
+
 /* cudaStream_t of the context (as void*), for events on the launching stream. */
 SWE_API void* swe_dev_stream(swe_dev_ctx* ctx);
 /* Device bytes held by the context. */

@@ -93,6 +93,7 @@ _SIGS = {
     "swe_dev_last_record": (c_int, [c_void_p, C.POINTER(swe_step_record), C.POINTER(swe_status)]),
     "swe_dev_run_ranks": (c_int, [c_void_p, c_int, c_ll, c_double, c_int]),
     "swe_dev_cell_skip": (c_int, [c_void_p, c_void_p]),
+    "swe_dev_cell_order": (c_int, [c_void_p, c_void_p]),
     "swe_dev_stream": (c_void_p, [c_void_p]),
     "swe_dev_memory_bytes": (c_ll, [c_void_p]),
     "swe_dev_launch_count": (c_ll, []),

@@ -434,13 +434,13 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
   int* c_new = const_cast<int*>(d.c_new);
   int* e_orig = const_cast<int*>(d.e_orig);
 
-  // 1. cells: space-filling-curve order (SWE_HILBERT) of the owned cells'
-  //    centroids (stable: ties keep
-  //    reference order); ghost cells keep their place after the owned ones
+  // 1. cells: blocked-Hilbert order of the owned cells' centroids (stable:
+  //    ties keep reference order); ghost cells keep their place after the
+  //    owned ones
   const int Co = d.C_own;
-  const bool morton = !(x->flags & SWE_FLAG_IDENTITY_ORDER) && m->cx && m->cy;
+  const bool curve = !(x->flags & SWE_FLAG_IDENTITY_ORDER) && m->cx && m->cy;
   if (ok) k_iota<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig);
-  if (ok && morton) {
+  if (ok && curve) {
     double x0 = m->cx[0], x1 = x0, y0 = m->cy[0], y1 = y0;
     for (int c = 1; c < Co; ++c) {
       x0 = std::min(x0, m->cx[c]);
@@ -453,19 +453,11 @@ int preprocess(swe_dev_ctx* x, const swe_mesh_view* m) {
     double* dcy = (double*)tmp.get(sizeof(double) * Co);
     ok = dcx && dcy && up(dcx, m->cx, sizeof(double) * Co) && up(dcy, m->cy, sizeof(double) * Co);
     if (ok) {
-#if SWE_HILBERT == 2
       const double side = std::max(std::min(x1 - x0, y1 - y0), span / 255.0) * (1.0 + 1e-9);
       k_hilbert_blocks<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
                                                           side > 0 ? side : 1.0,
                                                           (y1 - y0) > (x1 - x0), k64a, idx);
       ok = radix_sort(tmp, k64a, k64b, idx, c_orig, Co, 40, s);
-#else
-      unsigned* kin = (unsigned*)k64a;
-      unsigned* kout = (unsigned*)k64b;
-      k_morton<<<blocks_for(Co), kBlock, 0, s>>>(Co, dcx, dcy, x0, y0,
-                                                  span > 0 ? 65535.0 / span : 0.0, kin, idx);
-      ok = radix_sort(tmp, kin, kout, idx, c_orig, Co, 32, s);
-#endif
     }
   }
   if (ok) k_invert<<<blocks_for(C), kBlock, 0, s>>>(C, c_orig, c_new);
@@ -1874,6 +1866,12 @@ int swe_dev_built_export(swe_built_mesh* b, int* cell_nodes, double* area, doubl
 }
 
 void swe_dev_built_free(swe_built_mesh* b) { delete b; }
+
+int swe_dev_cell_order(swe_dev_ctx* x, int* order) {
+  if (!x || !order) return fail_invalid("swe_dev_cell_order: null argument");
+  CK(cudaMemcpy(order, x->d.c_orig, sizeof(int) * (size_t)x->d.C, cudaMemcpyDeviceToHost));
+  return SWE_OK;
+}
 
 int swe_dev_cell_skip(swe_dev_ctx* x, unsigned char* skipped) {
   if (!x || !skipped) return fail_invalid("swe_dev_cell_skip: null argument");

@@ -1,5 +1,5 @@
 // swe_prep.cuh -- device mesh preprocessor (run once per swe_dev_create):
-// space-filling-curve renumbering of cells (blocked Hilbert; Morton option),
+// space-filling-curve renumbering of cells (blocked Hilbert),
 // edge ordering by owner tile, the tile tables of the fused kernel, and the reference<->device permutation kernels.
 // The reference layout it consumes is build_mesh's (mesh.hpp:121-240);
 // orientation (left = reference left cell) and each cell's local edge order
@@ -10,22 +10,10 @@
 
 namespace swe_b200 {
 
-__device__ __forceinline__ unsigned spread16(unsigned v) {
-  v &= 0xffffu;
-  v = (v | (v << 8)) & 0x00ff00ffu;
-  v = (v | (v << 4)) & 0x0f0f0f0fu;
-  v = (v | (v << 2)) & 0x33333333u;
-  v = (v | (v << 1)) & 0x55555555u;
-  return v;
-}
-
-// cell order: SWE_HILBERT=2 (default) blocked Hilbert curve (k_hilbert_blocks);
-// 1 one Hilbert curve over the bounding square; 0 Morton (k_morton).  On
-// B200: 1M three-mound -16%, 10M dry bed -2.5%, 10M channel +0.8% step time
-// vs Morton
-#ifndef SWE_HILBERT
-#define SWE_HILBERT 2
-#endif
+// cell order: a blocked Hilbert curve (k_hilbert_blocks).  Measured on B200
+// against Morton and one Hilbert curve over the bounding square (both
+// removed): 1M three-mound -16%, 10M dry bed -2.5%, 10M channel +0.8% step
+// time vs Morton
 
 // 32-bit Hilbert index of (x, y) on a 65536^2 grid
 __device__ __forceinline__ unsigned hilbert16(unsigned x, unsigned y) {
@@ -46,22 +34,7 @@ __device__ __forceinline__ unsigned hilbert16(unsigned x, unsigned y) {
   return d;
 }
 
-// 32-bit Morton code of the centroid on a 65536^2 grid over the bounding box
-__global__ void k_morton(int C, const double* cx, const double* cy, double x0, double y0, double s,
-                         unsigned* key, int* idx) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  const double fx = fmin(fmax((cx[c] - x0) * s, 0.0), 65535.0);
-  const double fy = fmin(fmax((cy[c] - y0) * s, 0.0), 65535.0);
-#if SWE_HILBERT
-  key[c] = hilbert16((unsigned)fx, (unsigned)fy);
-#else
-  key[c] = spread16((unsigned)fx) | (spread16((unsigned)fy) << 1);
-#endif
-  idx[c] = c;
-}
-
-// SWE_HILBERT=2: the bounding box cut into squares along its long axis, each
+// The bounding box cut into squares along its long axis, each
 // traversed by a 65536^2 Hilbert curve (a curve ends at the corner where the
 // next square's begins); key = square index << 32 | Hilbert index (40 bits)
 __global__ void k_hilbert_blocks(int C, const double* cx, const double* cy, double x0, double y0,

@@ -71,3 +71,46 @@ def test_build_mesh_device_arguments_are_checked():
 def test_cell_skip_matches_info(solver):
     cs = solver.cell_skip()
     assert cs.dtype == np.uint8 and len(cs) == solver.n_cells and set(np.unique(cs)) <= {0, 1}
+
+
+def _hilbert16(x, y):
+    """d2xy's inverse on a 65536^2 grid (csrc/swe_prep.cuh hilbert16)"""
+    d, s = 0, 1 << 15
+    while s > 0:
+        rx, ry = (1 if x & s else 0), (1 if y & s else 0)
+        d += s * s * ((3 * rx) ^ ry)
+        if ry == 0:
+            if rx == 1:
+                x, y = 65535 - x, 65535 - y
+            x, y = y, x
+        s >>= 1
+    return d
+
+
+def test_cell_order_is_the_blocked_hilbert_curve():
+    """swe_dev_cell_order equals an independent restatement of the blocked-
+    Hilbert renumbering (squares of the short side along the long axis, a
+    65536^2 Hilbert curve in each, stable sort of 40-bit keys); it is a
+    permutation, square after square, and consecutive cells are neighbours
+    except where the curve crosses the thin last square."""
+    raw = api.generate_square_mesh(64, 16, 4.0, 1.0)  # 4:1 strip, cells of 1/16
+    m = api.build_mesh(raw, np.zeros(raw.n_cells), np.zeros(raw.n_cells))
+    s = api.DeviceSolver(m)
+    order = np.empty(m.n_cells, np.int32)
+    assert L.load().swe_dev_cell_order(s.ctx, L.ptr(order)) == L.SWE_OK
+    cx, cy = m.cx, m.cy
+    x0, x1, y0, y1 = cx.min(), cx.max(), cy.min(), cy.max()
+    side = max(min(x1 - x0, y1 - y0), max(x1 - x0, y1 - y0) / 255.0) * (1.0 + 1e-9)
+    keys = []
+    for c in range(m.n_cells):
+        a, b = (cx[c] - x0) / side, (cy[c] - y0) / side
+        blk = min(max(np.floor(a), 0.0), 255.0)
+        fx, fy = min(max((a - blk) * 65536.0, 0.0), 65535.0), min(max(b * 65536.0, 0.0), 65535.0)
+        keys.append((int(blk) << 32) | _hilbert16(int(fx), int(fy)))
+    want = np.argsort(np.array(keys, dtype=np.uint64), kind="stable")
+    assert np.array_equal(order, want)
+    assert np.array_equal(np.sort(order), np.arange(m.n_cells))
+    c = np.stack([cx, cy], 1)[order]
+    assert np.all(np.diff(np.floor((c[:, 0] - x0) / side)) >= 0)  # square after square
+    jumps = np.hypot(*np.diff(c, axis=0).T) * 16
+    assert (jumps > 2.0).sum() <= 2 and jumps.max() <= 8.0
