@@ -37,6 +37,26 @@
 
 namespace swe_b200 {
 
+// SWE_CHECKED=1 (test builds, tools/checked_build.sh): device-side bounds
+// checks of every index the step kernels compute -- tiles, cells, edges,
+// shared-memory slots, halo pushes -- trapping on a violation (this pool's
+// compute-sanitizer is closed; profiles/r02_sanitizer_closed.txt)
+#ifndef SWE_CHECKED
+#define SWE_CHECKED 0
+#endif
+#if SWE_CHECKED
+#define SWE_CHECK(cond)                                                              \
+  do {                                                                               \
+    if (!(cond)) {                                                                   \
+      printf("SWE_CHECK failed: %s (%s:%d) block %d thread %d\n", #cond, __FILE__,   \
+             __LINE__, (int)blockIdx.x, (int)threadIdx.x);                           \
+      __trap();                                                                      \
+    }                                                                                \
+  } while (0)
+#else
+#define SWE_CHECK(cond) ((void)0)
+#endif
+
 // per-thread accumulators of the cell update
 struct CellAcc {
   double lo, hi, mass, clip;
@@ -352,6 +372,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   int it = 0;
   for (int t = blockIdx.x; t < d.ntiles;) {
     const int c0 = t * T;
+    SWE_CHECK(t >= 0 && t < d.ntiles && c0 < d.C_own);
     const int nc = min(T, d.C_own - c0);
     const bool pre_skip = ahead && s_dec[it & 7] != 0;
     if (pre_skip) {
@@ -420,10 +441,12 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     // owned + halo edges -> contributions of the in-tile sides
     for (int j = threadIdx.x; j < (skip ? 0 : ns); j += NT) {
       const int e = j < no ? e0 + j : __ldg(d.halo + h0 + (j - no));
+      SWE_CHECK(e >= 0 && e < d.E);
       const int2 ek = SWE_LD_STREAM(d.ek + e);
       const double2 nn = SWE_LD_STREAM(d.enxy + e);
       const double nx = nn.x, ny = nn.y, len = SWE_LD_STREAM(d.len + e);
       const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
+      SWE_CHECK(cl < d.C && (ek.y == -1 || cr < d.C));
       const bool w = ek.y == -1;
       const int il = cl - c0, ir = (w ? cl : cr) - c0;
       const bool inL = (unsigned)il < (unsigned)nc, inR = !w && (unsigned)ir < (unsigned)nc;
@@ -463,6 +486,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
         if ((unsigned)il2 < (unsigned)nc) {
           const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
+          SWE_CHECK(s2 >= 0 && s2 < 3 * nc);
           const double ownL = (hg * uL.h) * uL.h;
           tm[s2] = f0 * len2;
           tx[s2] = (lx - ownL * nx) * len2;
@@ -470,6 +494,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         }
         if ((unsigned)ir2 < (unsigned)nc) {
           const int sr = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
+          SWE_CHECK(sr >= 0 && sr < 3 * nc);
           const double ownR = (hg * uR.h) * uR.h;
           tm[sr] = (-f0) * len2;  // right.mass = -f.mass
           tx[sr] = (rx - ownR * (-nx)) * len2;
@@ -526,6 +551,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     if (LINK && p1 > p0) {
       for (int j = p0 + threadIdx.x; j < p1; j += NT) {
         const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);
+        SWE_CHECK(i >= 0 && i < nc && g >= 0);
         double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + j) + 3 * (cur ^ 1);
         dst[0][g] = sh[i];
         dst[1][g] = sq[i];
@@ -756,10 +782,12 @@ __device__ __forceinline__ void run_tile_edges(const Dev& d, const double* H, co
   __syncthreads();
   for (int jj = threadIdx.x; jj < ns; jj += NT) {
     const int e = jj < no ? e0 + jj : __ldg(d.halo + h0 + (jj - no));
+    SWE_CHECK(e >= 0 && e < d.E);
     const int2 ek = __ldg(d.ek + e);
     const double2 nn = __ldg(d.enxy + e);
     const double nx = nn.x, ny = nn.y, len = __ldg(d.len + e);
     const int cl = ek.x & 0x3fffffff, cr = ek.y & 0x3fffffff;
+    SWE_CHECK(cl < d.C && (ek.y == -1 || cr < d.C));
     const bool w = ek.y == -1;
     const int il = cl - c0, ir = (w ? cl : cr) - c0;
     const bool inL = (unsigned)il < (unsigned)nc;
@@ -794,6 +822,7 @@ __device__ __forceinline__ void run_tile_edges(const Dev& d, const double* H, co
       const int il2 = (ek2.x & 0x3fffffff) - c0, ir2 = (ek2.y & 0x3fffffff) - c0;
       if ((unsigned)il2 < (unsigned)nc) {
         const int s2 = 3 * il2 + (int)((unsigned)ek2.x >> 30);
+        SWE_CHECK(s2 >= 0 && s2 < 3 * nc);
         const double ownL = (hg * uL.h) * uL.h;
         tm[s2] = f0 * len2;
         tx[s2] = (lx - ownL * nx) * len2;
@@ -801,6 +830,7 @@ __device__ __forceinline__ void run_tile_edges(const Dev& d, const double* H, co
       }
       if ((unsigned)ir2 < (unsigned)nc) {
         const int s3 = 3 * ir2 + (int)((unsigned)ek2.y >> 30);
+        SWE_CHECK(s3 >= 0 && s3 < 3 * nc);
         const double ownR = (hg * uR.h) * uR.h;
         tm[s3] = (-f0) * len2;
         tx[s3] = (rx - ownR * (-nx)) * len2;
@@ -890,6 +920,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
       }
       const int t = bid + j * nb;
       const int c0 = t * T;
+      SWE_CHECK(t >= 0 && t < d.ntiles && c0 < d.C_own);
       const int nc = min(T, d.C_own - c0);
       if (s_dec[j % kRunDec]) {
         // a run of consecutive skipped tiles (as k_tile's fast path): h kept,
@@ -964,6 +995,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
       if (LINK && p1 > p0) {
         for (int q = p0 + threadIdx.x; q < p1; q += NT) {
           const int i = __ldg(d.L.push_cell + q) - c0, g = __ldg(d.L.push_ghost + q);
+          SWE_CHECK(i >= 0 && i < nc && g >= 0);
           double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + q) + 3 * (cur ^ 1);
           dst[0][g] = sh[i];
           dst[1][g] = sq[i];
@@ -1095,6 +1127,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile_s(Dev d) 
 
   for (int t = blockIdx.x; t < d.ntiles; t += gridDim.x) {
     const int c0 = t * T;
+    SWE_CHECK(t >= 0 && t < d.ntiles && c0 < d.C_own);
     const int nc = min(T, d.C_own - c0);
     const int s0 = __ldg(d.soff + t), ns = __ldg(d.soff + t + 1) - s0;
     for (int i = threadIdx.x; i < nc; i += NT) {
@@ -1186,6 +1219,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_MINB * 256 / NT) k_tile_s(Dev d) 
     if (LINK && p1 > p0) {
       for (int j = p0 + threadIdx.x; j < p1; j += NT) {
         const int i = __ldg(d.L.push_cell + j) - c0, g = __ldg(d.L.push_ghost + j);
+        SWE_CHECK(i >= 0 && i < nc && g >= 0);
         double* const* dst = d.L.state + 6 * __ldg(d.L.push_rank + j) + 3 * (cur ^ 1);
         dst[0][g] = sh[i];
         dst[1][g] = sq[i];
