@@ -110,6 +110,40 @@ def measured_cost_weights(mesh: Mesh, state: FieldState, device: int = 0, steps:
         s.close()
 
 
+def refine_weights(weights, part, part_ms, damping: float = 0.8) -> np.ndarray:
+    """One rebalancing step from measured part step times: every cell of part
+    p is scaled by (t_p / mean t)^damping, so the next weighted RCB moves work
+    from slow parts to fast ones.  A few rounds equalise parts whose costs the
+    model misses (front tiles, halo edges, ramp / tail of short kernels)."""
+    t = np.asarray(part_ms, dtype=np.float64)
+    f = (t / t.mean()) ** damping
+    return np.asarray(weights, dtype=np.float64) * f[np.asarray(part)]
+
+
+def part_step_ms(mesh: Mesh, state: FieldState, part: np.ndarray, p: int, device: int = 0,
+                 steps: int = 40) -> float:
+    """Step time of part p alone (unlinked: its own dt), CUDA events on its
+    stream after a warm-up; the measurement behind refine_weights."""
+    import torch
+    lm = local_mesh(mesh, part, p)
+    lp = LinkedPart(lm, device=device)
+    try:
+        lp.set_state(state)
+        H = 1.7976931348623157e308
+        lp.advance(t_end=H, max_steps=5)
+        st = torch.cuda.ExternalStream(lp.lib.swe_dev_stream(lp.ctx), device=device)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(device)
+        e0.record(st)
+        lp.launch(t_end=H, max_steps=5 + steps)
+        e1.record(st)
+        torch.cuda.synchronize(device)
+        lp.records()
+        return e0.elapsed_time(e1) / steps
+    finally:
+        lp.close()
+
+
 @dataclass
 class LocalMesh:
     """One part's mesh in local numbering (owned first) + exchange plan."""
@@ -645,6 +679,6 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 4)
 
 
-__all__ = ["partition", "cost_weights", "measured_cost_weights", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
+__all__ = ["partition", "cost_weights", "measured_cost_weights", "refine_weights", "part_step_ms", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
            "run_lockstep", "run_ranks", "DeviceError", "LinkUnavailable"]

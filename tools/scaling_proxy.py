@@ -7,6 +7,8 @@ import json
 import sys
 from pathlib import Path
 
+import numpy as np
+
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
 
@@ -82,11 +84,19 @@ def main():
         cc = float(sys.argv[sys.argv.index("--measured") + 1]) \
             if len(sys.argv) > sys.argv.index("--measured") + 1 else None
         out["partition"] = f"cost-weighted RCB (measured skip pattern, computed tiles {cc}x)"
+    refine = int(sys.argv[sys.argv.index("--refine") + 1]) if "--refine" in sys.argv else 0
     for n in (2, 4, 8):
         if "--measured" in sys.argv:
             weights = dist.measured_cost_weights(mesh, sc.state, parts=n,
                                                  **({"computed_cost": cc} if cc else {}))
         part = dist.partition(mesh, n, weights)
+        history = []
+        for r in range(refine):  # rebalance from measured part times (dist.refine_weights)
+            pt = [dist.part_step_ms(mesh, sc.state, part, p, steps=40) for p in range(n)]
+            history.append(max(pt))
+            w0 = weights if weights is not None else np.ones(mesh.n_cells)
+            weights = dist.refine_weights(w0, part, pt)
+            part = dist.partition(mesh, n, weights)
         ts, cells, wet = [], [], []
         for p in range(n):
             lm = dist.local_mesh(mesh, part, p)
@@ -96,6 +106,8 @@ def main():
             cells.append(lm.n_owned)
             wet.append(float((sc.state.h[lm.cells[:lm.n_owned]] > 0).mean()))
             lp.close()
+        if refine:
+            out.setdefault("refine_history_ms_max", {})[n] = history
         mx = max(ts)
         exch = t1l - t1
         out[f"N{n}"] = {"ms_parts": ts, "owned_cells": cells, "wet_fraction": wet,
