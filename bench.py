@@ -65,9 +65,12 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0,
                     help="target CPU work of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--weak-base", type=int, default=2265,
+                    help="weak scaling: generator nx at N=1 (default: SURVEY's 2265)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
-                    help="N > 1: strong = the configured mesh split N ways; weak = N x the cells")
+                    help="N > 1: strong = the configured mesh split N ways; weak = BASELINE "
+                         "configs[4], the square water drop at ~10.26M cells per GPU")
     return ap.parse_args()
 
 
@@ -164,14 +167,15 @@ def build_workload(name, scale, device=None):
     return sc, mesh, time.perf_counter() - t0
 
 
-def produce_workload(name, scale):
+def produce_workload(name, scale, weak_nx=2265):
     """The same inputs from a producer SUBPROCESS (tools/make_workload.py), so
     the process that runs the reference never loads libswe_b200.so."""
     import tempfile
     with tempfile.TemporaryDirectory(prefix="swe_wl_") as d:
         out = Path(d) / "w.npz"
         subprocess.run([sys.executable, str(ROOT / "tools" / "make_workload.py"), "--config", name,
-                        "--scale", repr(scale), "--out", str(out)], check=True)
+                        "--scale", repr(scale), "--weak-nx", str(weak_nx), "--out", str(out)],
+                       check=True)
         with np.load(out) as z:
             return {k: z[k] for k in z.files}
 
@@ -255,8 +259,8 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable":
                           "oracle/_ref/libswe_ref.so was not built (needs /root/reference)"}))
         return
-    scale = args.scale * (world ** 0.5 if args.scaling == "weak" and world > 1 else 1.0)
-    wl = produce_workload(args.config, scale)
+    wl = (produce_workload("weak_square", 1.0, weak_nx=weak_nx(world)) if args.scaling == "weak"
+          else produce_workload(args.config, args.scale))
     rm, build_s = ref_mesh_of(wl)
     threads = reference_threads()
     # bounded sample: ~0.34 s per step at 10M cells on 16 threads, so at most
@@ -272,7 +276,7 @@ def run_reference(args):
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * r["phase_s"] / K, "higher_is_better": True,
            "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": workload_config(args.config, rm.n_cells, rm.n_edges, rm.n_boundary,
+           "config": workload_config(cfg_name(args), rm.n_cells, rm.n_edges, rm.n_boundary,
                                      args.gpus),
            "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": threads,
                             "kind": "reference", "sample": sample, "host": host_cpu_info()},
@@ -307,12 +311,27 @@ def run_b200_dist(args, rank, local, world):
     import torch.distributed as tdist
     from paper_1807_00672_b200 import api, dist
 
-    scale = args.scale * (world ** 0.5 if args.scaling == "weak" else 1.0)
-    sc, mesh, setup_s = build_workload(args.config, scale, device=local)
-    # equal work per GPU: cells weighted by the device's own dry-tile skip pattern
-    part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local,
-                                                                  parts=world))
-    lm = dist.local_mesh(mesh, part, rank)
+    if args.scaling == "weak":
+        # BASELINE configs[4] / SURVEY §8(d) 5: the square water drop at ~10.26M
+        # cells per GPU (nx = 2265, 3203, 4530, 6406 for N = 1, 2, 4, 8); every
+        # rank builds only its own part from the raw mesh (build_rank_mesh) --
+        # the global 82M-cell Mesh would need ~40 GB of host memory per rank
+        t0 = time.perf_counter()
+        nx = weak_nx(world)
+        sc = api.make_scenario("weak_square", weak_nx=nx)
+        part = dist.partition_raw(sc.raw, world)  # the drop is wet everywhere: equal counts
+        lm = dist.rank_mesh(sc.raw, sc.bed, sc.manning, part, rank)
+        mesh = None
+        C, E, NB = sc.raw.n_cells, 3 * nx * nx + 2 * nx, 4 * nx
+        setup_s = time.perf_counter() - t0
+    else:
+        scale = args.scale
+        sc, mesh, setup_s = build_workload(args.config, scale, device=local)
+        C, E, NB = mesh.n_cells, mesh.n_edges, mesh.n_boundary_edges
+        # equal work per GPU: cells weighted by the device's own dry-tile skip pattern
+        part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local,
+                                                                      parts=world))
+        lm = dist.local_mesh(mesh, part, rank)
     lp = dist.LinkedPart(lm, device=local)
     inf = api.DeviceSolver.info(lp)
     U = inf["graph_unroll"]  # steps per WHILE iteration (graph loop)
@@ -321,7 +340,7 @@ def run_b200_dist(args, rank, local, world):
         dist.link_torch(lp)
     except dist.LinkUnavailable as e:  # every rank takes this branch together
         lp.close()
-        return run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s,
+        return run_dist_host_driven(args, rank, local, world, sc, (C, E, NB), part, lm, setup_s,
                                     reason=str(e))
     lp.set_state(sc.state)
     horizon = HORIZON
@@ -380,12 +399,11 @@ def run_b200_dist(args, rank, local, world):
     tdist.all_reduce(sk, op=tdist.ReduceOp.SUM)
     skip_frac = float(sk[0].item()) / max(1.0, float(sk[1].item()))
     ms = float(ms.item())
-    C = mesh.n_cells
     # e2e: host state in, the same K steps, owned state back to the host
     # (the state at step W -- the window's start -- is re-formed untimed)
     lp.set_state(sc.state)
     advance(W)
-    start = api.FieldState.zeros(mesh.n_cells)
+    start = api.FieldState.zeros(C)
     t_start, _ = lp.gather_owned(start)
     gath = [None] * world
     tdist.all_gather_object(gath, (lm.cells[:lm.n_owned], start.h[lm.cells[:lm.n_owned]],
@@ -404,12 +422,11 @@ def run_b200_dist(args, rank, local, world):
         out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": workload_config(args.config, mesh.n_cells, mesh.n_edges,
-                                         mesh.n_boundary_edges, world),
+               "config": workload_config(cfg_name(args), C, E, NB, world),
                "decomposition": {
                    "how": f"{world}-way cost-weighted RCB domain decomposition (cells "
                           "of computed tiles weighted "
-                          f"{dist.COMPUTED_COST_LARGE if mesh.n_cells / world >= dist.LARGE_PART_CELLS else dist.COMPUTED_COST}"
+                          f"{dist.COMPUTED_COST_LARGE if C / world >= dist.LARGE_PART_CELLS else dist.COMPUTED_COST}"
                           "x cells of skipped dry tiles, measured on the device), one "
                           "part per GPU; "
                           "ghost states pushed peer-to-peer by the step kernel, CFL "
@@ -429,7 +446,7 @@ def run_b200_dist(args, rank, local, world):
                                      "(k_tile with halo push, k_exchange); steps past the stop "
                                      "exit at once"),
                "clocks": clk.summary() if clk else None,
-               "roofline": dist_roofline(mesh, K, ms, world, skip_frac),
+               "roofline": dist_roofline(C, E, K, ms, world, skip_frac),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
                        "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": (24 * C + 40 * K) / K,
                        "path": "LinkedPart.set_state (host) + advance (K steps, records D2H) + "
@@ -444,7 +461,7 @@ def run_b200_dist(args, rank, local, world):
     tdist.destroy_process_group()
 
 
-def run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s, reason):
+def run_dist_host_driven(args, rank, local, world, sc, sizes, part, lm, setup_s, reason):
     """Fallback when peer memory cannot be mapped (CUDA IPC unavailable): the
     host-driven protocol -- halo pack / NCCL send-recv / unpack, CFL bound by
     NCCL all_reduce, one step per round (dist.run_parts + TorchExchange)."""
@@ -476,7 +493,7 @@ def run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s, 
     ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     ms = float(ms.item())
-    C = mesh.n_cells
+    C, E, NB = sizes
     tdist.barrier()
     t0 = time.perf_counter()
     ps.set_state(sc.state)
@@ -489,8 +506,7 @@ def run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s, 
         out = {"metric": METRIC, "value": C * K / (ms / 1e3), "unit": UNIT, "n_gpus": world,
                "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
                "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "config": workload_config(args.config, mesh.n_cells, mesh.n_edges,
-                                         mesh.n_boundary_edges, world),
+               "config": workload_config(cfg_name(args), C, E, NB, world),
                "decomposition": {
                    "how": f"{world}-way cost-weighted RCB domain decomposition, host-"
                           "driven exchange (NCCL send/recv + all_reduce per step): "
@@ -502,7 +518,7 @@ def run_dist_host_driven(args, rank, local, world, sc, mesh, part, lm, setup_s, 
                                     "unpack, k_set_params, k_gate, k_tile, k_finalize (+ NCCL "
                                     "kernels, not counted)",
                "clocks": clk.summary() if clk else None,
-               "roofline": dist_roofline(mesh, K, ms, world, 0.0),
+               "roofline": dist_roofline(C, E, K, ms, world, 0.0),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
                        "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": 24 * C / K,
                        "path": "PartSolver.set_state (host) + K steps + gather_owned (host)"},
@@ -528,12 +544,25 @@ def lp_tiles(lp):
     return _lp_info(lp)[2]
 
 
-def dist_roofline(mesh, K, ms, world, skip_frac):
+WEAK_BASE = 2265
+
+
+def weak_nx(world):
+    """~10.26M cells per GPU (--weak-base shrinks it for checks)"""
+    if WEAK_BASE == 2265:
+        return {1: 2265, 2: 3203, 4: 4530, 8: 6406}.get(world, int(round(2265 * world ** 0.5)))
+    return int(round(WEAK_BASE * world ** 0.5))
+
+
+def cfg_name(args):
+    return "weak_square" if args.scaling == "weak" else args.config
+
+
+def dist_roofline(C, E, K, ms, world, skip_frac):
     """whole-job step roofline of an N-GPU run: SURVEY §8(d) canonical step
     bytes (skipped dry tiles at 40 B/cell) over the max-over-ranks step time,
     against N x the per-GPU HBM peak"""
     peak, src = load_peaks()
-    C, E = mesh.n_cells, mesh.n_edges
     step = (1.0 - skip_frac) * (116 * C + 128 * E) + skip_frac * 40 * C
     achieved = step / (ms / K / 1e3) / 1e9
     return {"bound": "hbm", "kernel": "step (all ranks)", "achieved": achieved,
@@ -814,7 +843,9 @@ def cpu_baseline(sc, mesh, args, W):
 
 
 def main():
+    global WEAK_BASE
     args = parse()
+    WEAK_BASE = args.weak_base
     if args.impl == "reference":
         run_reference(args)
     else:

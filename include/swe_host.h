@@ -64,6 +64,13 @@ SWE_API int swe_host_partition(void* mesh, int nparts, int* part_out);
 /* the same with per-cell weights (equal weight per part; include/swe/partition.hpp
  * cost_weights gives the step's measured cost of wet vs dry cells) */
 SWE_API int swe_host_partition_weighted(void* mesh, int nparts, const double* weights, int* part_out);
+/* RCB of a RAW mesh's triangle centroids (weights may be NULL) */
+SWE_API int swe_host_partition_raw(void* raw, int nparts, const double* weights, int* part_out);
+/* part p's local mesh built from the raw mesh alone (include/swe/multigpu.hpp
+ * build_rank_mesh: owned triangles + ghost layer; edge ids part-local);
+ * the same handle type as swe_host_local_mesh */
+SWE_API void* swe_host_rank_mesh(void* raw, const double* bed, const double* manning,
+                                 const int* part, int p, char* err, int errlen);
 /* part p's local mesh (owned cells first, then ghosts) and exchange plan */
 SWE_API void* swe_host_local_mesh(void* mesh, const int* part, int p, char* err, int errlen);
 SWE_API void swe_host_local_sizes(void* local, int* n_cells, int* n_owned, int* n_edges,

@@ -136,6 +136,9 @@ _SIGS = {
     "swe_host_partition": (c_int, [c_void_p, c_int, c_void_p]),
     "swe_host_partition_weighted": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
     "swe_host_local_mesh": (c_void_p, [c_void_p, c_void_p, c_int, c_char_p, c_int]),
+    "swe_host_partition_raw": (c_int, [c_void_p, c_int, c_void_p, c_void_p]),
+    "swe_host_rank_mesh": (c_void_p, [c_void_p, c_void_p, c_void_p, c_void_p, c_int, c_char_p,
+                                      c_int]),
     "swe_host_local_sizes": (None, [c_void_p] + [P_int] * 6),
     "swe_host_local_export": (None, [c_void_p] + [c_void_p] * 15),
     "swe_host_local_plan": (None, [c_void_p] + [c_void_p] * 5),

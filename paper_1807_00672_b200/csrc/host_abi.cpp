@@ -422,6 +422,33 @@ EXPORT int swe_host_partition_weighted(void* mp, int nparts, const double* weigh
   }
 }
 
+EXPORT int swe_host_partition_raw(void* rp, int nparts, const double* weights, int* part_out) {
+  try {
+    const auto& raw = *static_cast<swe::RawMesh*>(rp);
+    std::vector<double> w;
+    if (weights) w.assign(weights, weights + raw.triangles.size());
+    const std::vector<int> p = swe::rcb_partition(raw, nparts, weights ? &w : nullptr);
+    std::memcpy(part_out, p.data(), sizeof(int) * p.size());
+    return 0;
+  } catch (const std::exception& e) {
+    return kind_of(e);
+  }
+}
+
+EXPORT void* swe_host_rank_mesh(void* rp, const double* bed, const double* manning, const int* part,
+                                int p, char* err, int errlen) {
+  try {
+    const auto& raw = *static_cast<swe::RawMesh*>(rp);
+    const size_t nc = raw.triangles.size();
+    const std::vector<int> pv(part, part + nc);
+    const std::vector<double> b(bed, bed + nc), m(manning, manning + nc);
+    return new swe::LocalMesh(swe::build_rank_mesh(raw, b, m, pv, p));
+  } catch (const std::exception& e) {
+    put(e, err, errlen);
+    return nullptr;
+  }
+}
+
 EXPORT void* swe_host_local_mesh(void* mp, const int* part, int p, char* err, int errlen) {
   try {
     const auto& m = *static_cast<swe::Mesh*>(mp);

@@ -184,6 +184,35 @@ def local_mesh(mesh: Mesh, part: np.ndarray, p: int) -> LocalMesh:
     h = lib.swe_host_local_mesh(mesh.handle, L.ptr(part), p, err, len(err))
     if not h:
         _raise(3, err.value)
+    return _local_from_handle(lib, h, p)
+
+
+def partition_raw(raw, nparts: int, weights=None) -> np.ndarray:
+    """RCB over a RAW mesh's triangle centroids (no global Mesh needed)."""
+    out = np.empty(raw.n_cells, dtype=np.int32)
+    w = None if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    rc = L.load().swe_host_partition_raw(raw.handle, nparts, L.ptr(w), L.ptr(out))
+    if rc:
+        _raise(rc, "rcb_partition (raw) failed")
+    return out
+
+
+def rank_mesh(raw, bed, manning, part: np.ndarray, p: int) -> LocalMesh:
+    """Part p's LocalMesh built from the raw mesh alone (owned triangles +
+    ghost layer; include/swe/multigpu.hpp build_rank_mesh): a rank of a large
+    run never materialises the global Mesh.  Edge ids are part-local."""
+    lib = L.load()
+    part = np.ascontiguousarray(part, dtype=np.int32)
+    b = np.ascontiguousarray(bed, dtype=np.float64)
+    m = np.ascontiguousarray(manning, dtype=np.float64)
+    err = _errbuf()
+    h = lib.swe_host_rank_mesh(raw.handle, L.ptr(b), L.ptr(m), L.ptr(part), p, err, len(err))
+    if not h:
+        _raise(3, err.value)
+    return _local_from_handle(lib, h, p)
+
+
+def _local_from_handle(lib, h, p: int) -> LocalMesh:
     try:
         s = [C.c_int() for _ in range(6)]
         lib.swe_host_local_sizes(h, *[C.byref(x) for x in s])
@@ -679,6 +708,6 @@ def run_parts(parts, exchange, nsteps: int, t_end: float = 1e30):
     return np.array(out, dtype=np.float64).reshape(-1, 4)
 
 
-__all__ = ["partition", "cost_weights", "measured_cost_weights", "refine_weights", "part_step_ms", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
+__all__ = ["partition", "cost_weights", "measured_cost_weights", "refine_weights", "part_step_ms", "partition_raw", "rank_mesh", "local_mesh", "LocalMesh", "PartSolver", "LocalExchange", "TorchExchange",
            "run_parts", "push_plan", "LinkedPart", "link_local", "link_torch", "exchange_link_info",
            "run_lockstep", "run_ranks", "DeviceError", "LinkUnavailable"]

@@ -26,11 +26,12 @@ def main() -> None:
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", required=True)
     ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--weak-nx", type=int, default=2265)
     ap.add_argument("--out", required=True)
     a = ap.parse_args()
     from paper_1807_00672_b200 import api
     t0 = time.perf_counter()
-    sc = api.make_scenario(a.config, scale=a.scale, unstructured=True)
+    sc = api.make_scenario(a.config, scale=a.scale, unstructured=True, weak_nx=a.weak_nx)
     np.savez(a.out, nodes=sc.raw.nodes, tris=sc.raw.triangles, bed=sc.bed, manning=sc.manning,
              h=sc.state.h, qx=sc.state.qx, qy=sc.state.qy, t_end=np.float64(sc.t_end),
              gen_s=np.float64(time.perf_counter() - t0))
