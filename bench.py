@@ -663,6 +663,8 @@ def run_b200(args):
     step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical B_step
     step_eff = (1.0 - skip_frac) * step_bytes + skip_frac * 40 * C  # skipped tiles: 40 B/cell
     prof = load_traffic()
+    if prof.get("config", "channel") != args.config or args.scale != 1.0:
+        prof = {}  # the committed capture is of another mesh: no per-launch bytes for this one
     if info["fused"]:
         # the dominant kernel k_tile does the whole step (face + cell work of
         # §8(d)) in one launch: its algorithmic bytes per launch are B_step,
