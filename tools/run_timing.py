@@ -21,10 +21,19 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="channel")
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--steps", type=int, default=200)
+ap.add_argument("--parts", type=int, default=1, help="time part 0 of an N-way RCB split")
 a = ap.parse_args()
 sc = api.make_scenario(a.config, scale=a.scale)
 m = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
-s = api.DeviceSolver(m)
+if a.parts > 1:
+    from paper_1807_00672_b200 import dist
+    part = dist.partition(m, a.parts)
+    s = dist.LinkedPart(dist.local_mesh(m, part, 0))  # unlinked: its own dt
+    s.stream = s.lib.swe_dev_stream(s.ctx)
+    s.info = lambda: api.DeviceSolver.info(s)
+    s.advance_async = lambda t_end, max_steps: s.launch(t_end=t_end, max_steps=max_steps)
+else:
+    s = api.DeviceSolver(m)
 s.set_state(sc.state)
 s.advance(1e300, max_steps=300)  # clocks
 s.set_state(sc.state)
