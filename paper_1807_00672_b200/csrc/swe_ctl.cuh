@@ -174,6 +174,7 @@ struct Dev {
   Sync* sync;
   int* pflag;
   const unsigned char* tile_ghost;
+  int run_noacq;  // no L1-invalidating acquire per step (state via ld.cg only)
   const int *sel, *ser, *skk, *sedge;  // cells, kl | kr << 8, device edge (error path)
   const double *snx, *sny, *slen;
   // state, double-buffered

@@ -872,7 +872,10 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
       if (it > 0) {  // relaxed polls (an acquire per poll would flush L1 each time)
         const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
         poll_until(&sy->epoch, it);
-        fence_acq_rel_gpu();  // acquire the commit (and the peers' halo pushes)
+        // acquire the commit (and the peers' halo pushes); run_noacq: the
+        // state is read through L2 only (ld.cg after the observed epoch, as
+        // before it), so L1 keeps the geometry across steps
+        if (!d.run_noacq) fence_acq_rel_gpu();
         RUN_T(1, global_ns() - w0);
       }
       s_cur = __ldcg(&ctl->cur);
@@ -940,7 +943,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
           const int ck = (t + k * nb) * T;
           const int nk = min(T, d.C_own - ck);
           for (int i = threadIdx.x; i < nk; i += NT) {
-            const double h = H[ck + i];
+            const double h = __ldcg(H + ck + i);
             NH[ck + i] = h;
             NQX[ck + i] = 0.0;
             NQY[ck + i] = 0.0;
@@ -956,7 +959,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
         viewed = true;
         dt = s_dt;
       }
-      if (viewed)
+      if (viewed && (it == 0 || !d.run_noacq))
         run_tile_edges<NT, false>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
       else  // before the epoch: L1 may hold this buffer from two steps ago
         run_tile_edges<NT, true>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
