@@ -111,9 +111,19 @@ struct Link {
 // arrivals at the end of every step (monotonic within a launch); the last to
 // arrive commits the step and publishes it as the next epoch.  k_gate resets
 // both before a launch.  One 128-byte line.
+// the committed view the workers need to update a step: published by the
+// control CTA as ONE 16-byte store after its commit, polled by the workers
+// with one 16-byte load (epoch, stop flag and the step's dt together: one
+// round trip instead of a poll and then the control block's fields)
+struct __align__(16) View {
+  unsigned int epoch;
+  int active;
+  double dt;
+};
+
 struct __align__(128) Sync {
   unsigned int arrive;
-  unsigned int epoch;
+  View view;
   // the step's CFL bound and max speed (bits of non-negative doubles, so
   // integer atomicMin / atomicMax order them exactly), double-buffered by
   // step parity: min and max are order-independent, so the workers fold them
@@ -225,6 +235,24 @@ __device__ __forceinline__ void poll_until(const unsigned int* p, unsigned int v
     __nanosleep(ns);
     ns = ns < 1024 ? 2 * ns : 1024;
   }
+}
+
+__device__ __forceinline__ void view_load(const View* v, unsigned int& epoch, int& active,
+                                          double& dt) {
+  unsigned long long a, b;
+  asm volatile("ld.volatile.global.v2.u64 {%0, %1}, [%2];" : "=l"(a), "=l"(b) : "l"(v) : "memory");
+  epoch = (unsigned int)a;
+  active = (int)(a >> 32);
+  dt = __longlong_as_double((long long)b);
+}
+
+// after a fence: the commit's stores are ordered before the view
+__device__ __forceinline__ void view_publish(View* v, unsigned int epoch, int active, double dt) {
+  const unsigned long long a =
+      (unsigned long long)epoch | ((unsigned long long)(unsigned int)active << 32);
+  const unsigned long long b = (unsigned long long)__double_as_longlong(dt);
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  asm volatile("st.volatile.global.v2.u64 [%0], {%1, %2};" ::"l"(v), "l"(a), "l"(b) : "memory");
 }
 
 __device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
@@ -411,7 +439,7 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   c->n_rec = 0;
   if (d.sync) {  // the persistent kernel's barrier starts over with every launch
     d.sync->arrive = 0;
-    d.sync->epoch = 0;
+    d.sync->view.epoch = 0;
     for (int k = 0; k < 2; ++k) {
       d.sync->lo[k] = 0x7ff0000000000000ULL;  // +inf
       d.sync->hi[k] = 0ULL;                   // +0

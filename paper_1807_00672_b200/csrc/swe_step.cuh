@@ -689,8 +689,8 @@ __device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
       if (threadIdx.x == 0) {
         s_c.step = __ldcg(&d.ctl->step);
         s_go = __ldcg(&d.ctl->active);
-        __threadfence();
-        st_release_gpu(&sy->epoch, it + 1);
+        const double t = __ldcg(&d.ctl->t), dts = __ldcg(&d.ctl->dts);
+        view_publish(&sy->view, it + 1, s_go, (t + dts >= s_sp.t_end) ? s_sp.t_end - t : dts);
       }
       __syncthreads();
       if (!s_go) return;
@@ -723,7 +723,9 @@ __device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
       store_commit(d.ctl, c);
       s_c = c;
       s_ci = ci;
-      st_release_gpu(&sy->epoch, it + 1);  // (a release: orders the stores above)
+      // the next step's dt as the workers' step_dt forms it (engine.hpp:236-237)
+      view_publish(&sy->view, it + 1, s_go,
+                   (c.t + c.dts >= s_sp.t_end) ? s_sp.t_end - c.t : c.dts);
       RUN_T(3, global_ns() - c0);
       RUN_T(5, 1);
       RUN_T(2, c0 - w0);
@@ -871,18 +873,29 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
     if (threadIdx.x == 0) {
       if (it > 0) {  // relaxed polls (an acquire per poll would flush L1 each time)
         const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
-        poll_until(&sy->epoch, it);
+        unsigned int e, ns = 32;
+        int act;
+        double dtv;
+        for (;;) {
+          view_load(&sy->view, e, act, dtv);
+          if (e >= it) break;
+          __nanosleep(ns);
+          ns = ns < 1024 ? 2 * ns : 1024;
+        }
         // acquire the commit (and the peers' halo pushes); run_noacq: the
         // state is read through L2 only (ld.cg after the observed epoch, as
         // before it), so L1 keeps the geometry across steps
         if (!d.run_noacq) fence_acq_rel_gpu();
+        s_active = act;
+        s_dt = dtv;
         RUN_T(1, global_ns() - w0);
+      } else {  // the launch's first step: the control block as the gate left it
+        s_cur = __ldcg(&ctl->cur);
+        s_step = __ldcg(&ctl->step);
+        s_active = __ldcg(&ctl->active);
+        const double t = __ldcg(&ctl->t), dts = __ldcg(&ctl->dts), t_end = __ldcg(&d.sp->t_end);
+        s_dt = (t + dts >= t_end) ? t_end - t : dts;  // engine.hpp:236-237 (step_dt)
       }
-      s_cur = __ldcg(&ctl->cur);
-      s_step = __ldcg(&ctl->step);
-      s_active = __ldcg(&ctl->active);
-      const double t = __ldcg(&ctl->t), dts = __ldcg(&ctl->dts), t_end = __ldcg(&d.sp->t_end);
-      s_dt = (t + dts >= t_end) ? t_end - t : dts;  // engine.hpp:236-237 (step_dt)
     }
     __syncthreads();
     return s_active != 0;
@@ -916,10 +929,12 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
     }
     for (int j = 0; j < ntl;) {
       if (j % kRunDec == 0) {  // skip decisions of the next chunk of tiles
+        const unsigned long long q0 = SWE_RUN_TIMING && j == 0 ? global_ns() : 0;
         __syncthreads();
         for (int k = threadIdx.x; k < kRunDec && j + k < ntl; k += NT)
           s_dec[k] = d.skip && run_skip(d, fl, bid + (j + k) * nb, tag);
         __syncthreads();
+        if (SWE_RUN_TIMING && j == 0 && threadIdx.x == 0) RUN_T(8, global_ns() - q0);
       }
       const int t = bid + j * nb;
       const int c0 = t * T;
@@ -959,16 +974,21 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
         viewed = true;
         dt = s_dt;
       }
+      const unsigned long long q1 = SWE_RUN_TIMING && j == 0 ? global_ns() : 0;
       if (viewed && (it == 0 || !d.run_noacq))
         run_tile_edges<NT, false>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
       else  // before the epoch: L1 may hold this buffer from two steps ago
         run_tile_edges<NT, true>(d, H, QX, QY, t, c0, nc, sh, sq, sr, sz, tm, tx, ty);
       __syncthreads();
+      const unsigned long long q2 = SWE_RUN_TIMING && j == 0 ? global_ns() : 0;
+      if (SWE_RUN_TIMING && j == 0 && threadIdx.x == 0) RUN_T(9, q2 - q1);
       if (!viewed) {  // the first computed tile's edges are done: now dt / stop
         if (!read_view(it)) return;
         viewed = true;
         dt = s_dt;
       }
+      const unsigned long long q3 = SWE_RUN_TIMING && j == 0 ? global_ns() : 0;
+      if (SWE_RUN_TIMING && j == 0 && threadIdx.x == 0) RUN_T(10, q3 - q2);
       int p0 = 0, p1 = 0;
       if (LINK) {
         p0 = __ldg(d.L.tile_push + t);
@@ -994,6 +1014,7 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
         }
       }
       dry = __syncthreads_and(dry);
+      if (SWE_RUN_TIMING && j == 0 && threadIdx.x == 0) RUN_T(11, global_ns() - q3);
       if (threadIdx.x == 0 && d.skip) __stcg(fl_next + t, dry ? tag + 1 : 0);
       if (LINK && p1 > p0) {
         for (int q = p0 + threadIdx.x; q < p1; q += NT) {

@@ -40,8 +40,8 @@ s.set_state(sc.state)
 s.advance(1e300, max_steps=5)
 lib = s.lib
 lib.swe_dev_run_timing.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
-v = (C.c_longlong * 9)()
-lib.swe_dev_run_timing(s.ctx, v, 9)  # clear
+v = (C.c_longlong * 12)()
+lib.swe_dev_run_timing(s.ctx, v, 12)  # clear
 st = torch.cuda.ExternalStream(s.stream, device=0)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 torch.cuda.synchronize()
@@ -51,12 +51,16 @@ e1.record(st)
 torch.cuda.synchronize()
 s.records()
 ms = e0.elapsed_time(e1)
-lib.swe_dev_run_timing(s.ctx, v, 9)
-work, ew, cw, com, cs, nc, aw, fin, red = list(v)
+lib.swe_dev_run_timing(s.ctx, v, 12)
+work, ew, cw, com, cs, nc, aw, fin, q_dec, q_edge, q_view, q_upd = list(v)
 print(json.dumps({"config": a.config, "us_per_step": 1e3 * ms / a.steps, "info": s.info(),
                   "per_cta_step_us": {"work_incl_epoch_wait": work / max(cs, 1) / 1e3,
                                       "epoch_wait": ew / max(cs, 1) / 1e3,
                                       "arrival_wait": aw / max(cs, 1) / 1e3},
+                  "first_tile_us": {"decisions": q_dec / max(cs, 1) / 1e3,
+                                    "stage_edges": q_edge / max(cs, 1) / 1e3,
+                                    "view": q_view / max(cs, 1) / 1e3,
+                                    "update": q_upd / max(cs, 1) / 1e3},
                   "commit_us": com / max(nc, 1) / 1e3,
-                  "control_wait_us": cw / max(nc, 1) / 1e3, "reduce_us": red / max(nc, 1) / 1e3,
+                  "control_wait_us": cw / max(nc, 1) / 1e3,
                   "deferred_us": fin / max(nc, 1) / 1e3, "cta_steps": cs, "commits": nc}))
