@@ -319,9 +319,56 @@ __device__ __forceinline__ CellGeo ldg_geo(const CellGeo* p) {
       : "l"(p));
   return g;
 }
+// SWE_TILE_TMA=1 (experiment build, tools/variant_build.sh): the tile's state
+// arrives by TMA bulk copies (cp.async.bulk + mbarrier complete_tx) into one of
+// two shared buffers, the next computed tile's copy issued when a tile starts,
+// so it lands while the current tile is evaluated.  16T doubles of shared
+// memory: 7 CTAs per SM at T = 224.
+#ifndef SWE_TILE_TMA
+#define SWE_TILE_TMA 0
+#endif
 __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
-  return sizeof(double) * 13 * (size_t)T + 0 * (size_t)S;  // state+bed [4T], contributions [9T]
+  // state+bed [4T], contributions [9T] (TMA: two state buffers [6T] + bed [T])
+  // (SWE_TILE_TMA=2: one buffer, the tile's own copy only: 13T, 8 CTAs per SM)
+  return sizeof(double) * (SWE_TILE_TMA == 1 ? 16 : 13) * (size_t)T + 0 * (size_t)S;
 }
+
+#if SWE_TILE_TMA
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  unsigned done;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// one tile's h / qx / qy (3 x bytes) into dst[0..3T): issued by one thread
+__device__ __forceinline__ void tma_state(double* dst, int T, const double* H, const double* QX,
+                                          const double* QY, int c0, unsigned bytes,
+                                          unsigned long long* bar) {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // after generic reads of dst
+  const unsigned b = smem_u32(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(3 * bytes)
+               : "memory");
+  const double* src[3] = {H + c0, QX + c0, QY + c0};
+#pragma unroll
+  for (int k = 0; k < 3; ++k)
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst + k * T)),
+        "l"(src[k]), "r"(bytes), "r"(b)
+        : "memory");
+}
+#endif
 
 // LINK: linked context -- after the update, push the tile's cells that peers
 // hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
@@ -329,7 +376,11 @@ __host__ __device__ constexpr size_t tile_smem_bytes(int T, int S) {
 // measured slower: its register copies spill into the main loop.)
 template <int NT, bool LINK>
 #ifndef SWE_TILE_BLOCKS
+#if SWE_TILE_TMA == 1
+#define SWE_TILE_BLOCKS(NT) (896 / (NT))
+#else
 #define SWE_TILE_BLOCKS(NT) (SWE_TILE_MINB * 256 / (NT))
+#endif
 #endif
 __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   extern __shared__ double smem[];
@@ -344,10 +395,24 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   double* NQX = d.qx[cur ^ 1];
   double* NQY = d.qy[cur ^ 1];
   const int T = d.T;
+#if SWE_TILE_TMA
+  double* const tbuf = smem;  // [2][3T]: the tile's state / the next computed tile's
+  double *sh = tbuf, *sq = sh + T, *sr = sq + T;
+  double* sz = smem + (SWE_TILE_TMA == 1 ? 6 : 3) * T;
+  __shared__ __align__(8) unsigned long long s_bar[2];
+  if (threadIdx.x == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  unsigned ph = 0;  // bit b: parity of buffer b's next completion
+  int pf_tile = -1, pf_buf = 0;
+#else
   double* sh = smem;
   double* sq = sh + T;
   double* sr = sq + T;
   double* sz = sr + T;
+#endif
   double* tm = sz + T;
   double* tx = tm + 3 * T;
   double* ty = tx + 3 * T;
@@ -405,6 +470,42 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       it += run;
       continue;
     }
+#if SWE_TILE_TMA
+    const bool full = nc == T;  // T * 8 bytes: a multiple of 16
+    int cb = 0;
+    if (pf_tile == t) {
+      cb = pf_buf;
+    } else if (full && threadIdx.x == 0) {
+      tma_state(tbuf, T, H, QX, QY, c0, (unsigned)(T * sizeof(double)), &s_bar[0]);
+    }
+    sh = tbuf + cb * 3 * T;
+    sq = sh + T;
+    sr = sq + T;
+    {  // the next tile's state (if it is computed), in flight during this one
+      const int tn = t + gridDim.x;
+      pf_tile = -1;
+      if (SWE_TILE_TMA == 1 && tn < d.ntiles && (tn + 1) * T <= d.C_own &&
+          !(ahead && s_dec[(it + 1) & 7])) {
+        if (threadIdx.x == 0)
+          tma_state(tbuf + (cb ^ 1) * 3 * T, T, H, QX, QY, tn * T, (unsigned)(T * sizeof(double)),
+                    &s_bar[cb ^ 1]);
+        pf_tile = tn;
+        pf_buf = cb ^ 1;
+      }
+    }
+    for (int i = threadIdx.x; i < nc; i += NT) {
+      if (!full) {  // the last, partial tile: plain loads
+        sh[i] = SWE_LD_STATE(H + c0 + i);
+        sq[i] = SWE_LD_STATE(QX + c0 + i);
+        sr[i] = SWE_LD_STATE(QY + c0 + i);
+      }
+      sz[i] = ldg_geo(d.cg + c0 + i).z;
+    }
+    if (full) {
+      mbar_wait(&s_bar[cb], (ph >> cb) & 1u);
+      ph ^= 1u << cb;
+    }
+#else
     for (int i = threadIdx.x; i < nc; i += NT) {  // stage the tile (a skipped one needs h only)
       sh[i] = SWE_LD_STATE(H + c0 + i);
       if (!pre_skip) {
@@ -413,6 +514,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         sz[i] = ldg_geo(d.cg + c0 + i).z;  // area, n, r come along (read at the update)
       }
     }
+#endif
     const int e0 = __ldg(d.eoff + t), no = __ldg(d.eoff + t + 1) - e0;
     const int h0 = __ldg(d.hoff + t), ns = no + __ldg(d.hoff + t + 1) - h0;
     int p0 = 0, p1 = 0;  // push-list range of the tile (linked)
