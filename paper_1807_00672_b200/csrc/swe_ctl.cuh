@@ -88,9 +88,17 @@ struct XPost {  // one rank's contribution to one exchange
   double err_h;   // depth of the blown-up cell (BLOWUP)
 };
 
+struct XSums {  // one rank's deferred sums (persistent kernel: posted after the commit)
+  double mass, clip;
+  long long events;
+  unsigned long long tag;
+};
+
 struct Mailbox {
   unsigned long long flag[kMaxRanks];  // flag[q]: last tag rank q posted here
   XPost slot[2][kMaxRanks];            // [tag & 1][q]
+  unsigned long long dflag[kMaxRanks];  // dflag[q]: last tag of rank q's deferred sums
+  XSums sums[2][kMaxRanks];
 };
 
 struct Link {
@@ -662,12 +670,18 @@ __device__ void post_outcome(const Dev& d, const Part& p, int kind) {
   __syncwarp();
 }
 
-// wait for every rank's post, combine in rank order, commit (one warp)
-__device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHandle cond,
-                                int use_cond) {
+// wait for every rank's post of exchange `tag` and combine them in rank order
+// (one warp; every lane ends with the same result)
+struct XCombined {
+  Part g;
+  int neg, blow, bad;
+  double err_h;
+  bool timeout;
+};
+
+__device__ XCombined wait_combine(const Dev& d, unsigned long long tag) {
   const int lane = threadIdx.x & 31;
   const Link& L = d.L;
-  const unsigned long long tag = __ldcg(&d.ctl->xseq);
   Mailbox* m = L.mine;
   const unsigned long long t0 = global_ns();
   bool timeout = false;
@@ -680,9 +694,12 @@ __device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHand
       __nanosleep(64);
     }
   // combine in rank order: every rank forms the same sums
-  Part g{INFINITY, 0.0, 0.0, 0.0, 0, 0};
-  int neg = kNone, blow = kNone, bad = kNone;
-  double err_h = 0.0;
+  XCombined r;
+  r.g = Part{INFINITY, 0.0, 0.0, 0.0, 0, 0};
+  r.neg = kNone;
+  r.blow = kNone;
+  r.bad = kNone;
+  r.err_h = 0.0;
   for (int base = 0; base < L.nranks; base += 32) {
     const int q = base + lane;
     XPost s{};
@@ -711,40 +728,148 @@ __device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHand
       const int ix = __shfl_sync(0xffffffffu, s.index, j);
       const int bs = __shfl_sync(0xffffffffu, s.bad_speed, j);
       const double eh = __shfl_sync(0xffffffffu, s.err_h, j);
-      g.lo = sel_min(g.lo, lo);
-      g.hi = sel_max(g.hi, hi);
-      g.mass += ms;
-      g.clip += cl;
-      g.events += ev;
-      if (st == SWE_NEGATIVE_DEPTH) neg = min(neg, ix);
-      if (st == SWE_BLOWUP && ix < blow) {
-        blow = ix;
-        err_h = eh;
+      r.g.lo = sel_min(r.g.lo, lo);
+      r.g.hi = sel_max(r.g.hi, hi);
+      r.g.mass += ms;
+      r.g.clip += cl;
+      r.g.events += ev;
+      if (st == SWE_NEGATIVE_DEPTH) r.neg = min(r.neg, ix);
+      if (st == SWE_BLOWUP && ix < r.blow) {
+        r.blow = ix;
+        r.err_h = eh;
       }
-      bad = min(bad, bs);
+      r.bad = min(r.bad, bs);
     }
   }
-  timeout = __any_sync(0xffffffffu, timeout);
+  r.timeout = __any_sync(0xffffffffu, timeout);
+  return r;
+}
+
+__device__ __forceinline__ void link_timeout(Ctl* c) {
+  c->link_err = 1;
+  c->status = SWE_NCCL;
+  c->err_index = -1;
+  c->active = 0;
+  c->cfl_valid = 0;
+}
+
+// wait for every rank's post, combine in rank order, commit (one warp)
+__device__ void wait_and_commit(const Dev& d, int kind, cudaGraphConditionalHandle cond,
+                                int use_cond) {
+  const int lane = threadIdx.x & 31;
+  const XCombined r = wait_combine(d, __ldcg(&d.ctl->xseq));
   if (lane != 0) return;
   Ctl* c = d.ctl;
-  if (timeout) {
-    c->link_err = 1;
-    c->status = SWE_NCCL;
-    c->err_index = -1;
-    c->active = 0;
-    c->cfl_valid = 0;
+  if (r.timeout) {
+    link_timeout(c);
     if (use_cond) cudaGraphSetConditional(cond, 0);
     return;
   }
-  c->bad_speed = bad;
+  c->bad_speed = r.bad;
   if (kind == 1) {
     Ctl v = load_ctl(c);
-    set_cfl_cache(&v, g, d.P);
+    set_cfl_cache(&v, r.g, d.P);
     *c = v;
     return;
   }
-  const int status = neg != kNone ? SWE_NEGATIVE_DEPTH : (blow != kNone ? SWE_BLOWUP : SWE_OK);
-  finalize_step(d, g, status, status == SWE_NEGATIVE_DEPTH ? neg : blow, err_h, cond, use_cond);
+  const int status =
+      r.neg != kNone ? SWE_NEGATIVE_DEPTH : (r.blow != kNone ? SWE_BLOWUP : SWE_OK);
+  finalize_step(d, r.g, status, status == SWE_NEGATIVE_DEPTH ? r.neg : r.blow, r.err_h, cond,
+                use_cond);
+}
+
+// ---- the persistent kernel's split exchange (linked ranks) -----------------
+// The step's commit needs only the CFL bound, the max speed and the error
+// slots: the control CTA posts those as soon as its workers have arrived
+// (bound and speed folded in by the workers' atomics), commits the head
+// (clock, buffer, stop) from the combined posts and publishes it; the mass /
+// clip sums follow in a second post (sums[], dflag[]) once reduced, and the
+// record / ledger are completed from their rank-order combination.
+
+// the head: wait + combine the critical posts, commit_head (warp 0; lane 0
+// holds go and ci).  Returns go (0 on timeout: the loop stops)
+__device__ int wait_commit_head(const Dev& d, const StepParams& sp, CommitInfo& ci, bool& tmo) {
+  const int lane = threadIdx.x & 31;
+  const XCombined r = wait_combine(d, __ldcg(&d.ctl->xseq));
+  tmo = r.timeout;
+  int go = 0;
+  if (lane == 0) {
+    if (r.timeout) {
+      link_timeout(d.ctl);
+      ci.ok = false;
+    } else {
+      Ctl c = load_ctl(d.ctl);
+      c.bad_speed = r.bad;
+      const int status =
+          r.neg != kNone ? SWE_NEGATIVE_DEPTH : (r.blow != kNone ? SWE_BLOWUP : SWE_OK);
+      go = commit_head(c, sp, r.g.lo, r.g.hi, status,
+                       status == SWE_NEGATIVE_DEPTH ? r.neg : r.blow, r.err_h, d.P, ci);
+      store_commit(d.ctl, c);
+    }
+  }
+  return __shfl_sync(0xffffffffu, go, 0);
+}
+
+// the tail: post this rank's sums, wait for every rank's, combine in rank
+// order, complete the record and the ledger (warp 0).  Returns 0 on timeout.
+__device__ int post_wait_sums(const Dev& d, const StepParams& sp, const Part& p,
+                              const CommitInfo& ci) {
+  const int lane = threadIdx.x & 31;
+  const Link& L = d.L;
+  const unsigned long long tag = __ldcg(&d.ctl->xseq);
+  XSums x;
+  x.mass = p.mass;
+  x.clip = p.clip;
+  x.events = p.events;
+  x.tag = tag;
+  __syncwarp();
+  for (int q = lane; q < L.nranks; q += 32) {
+    L.box[q]->sums[tag & 1][L.rank] = x;
+    st_release_sys(&L.box[q]->dflag[L.rank], tag);
+  }
+  Mailbox* m = L.mine;
+  const unsigned long long t0 = global_ns();
+  bool timeout = false;
+  for (int q = lane; q < L.nranks && !timeout; q += 32)
+    while (ld_acquire_sys(&m->dflag[q]) < tag) {
+      if (global_ns() - t0 > L.timeout_ns) {
+        timeout = true;
+        break;
+      }
+      __nanosleep(64);
+    }
+  Part g{INFINITY, 0.0, 0.0, 0.0, 0, 0};
+  for (int base = 0; base < L.nranks; base += 32) {
+    const int q = base + lane;
+    double ms = 0.0, cl = 0.0;
+    long long ev = 0;
+    if (q < L.nranks && !timeout) {
+      const volatile XSums* v = &m->sums[tag & 1][q];
+      ms = v->mass;
+      cl = v->clip;
+      ev = v->events;
+      if (v->tag != tag) timeout = true;
+    }
+    const int cnt = min(32, L.nranks - base);
+    for (int j = 0; j < cnt; ++j) {
+      g.mass += __shfl_sync(0xffffffffu, ms, j);
+      g.clip += __shfl_sync(0xffffffffu, cl, j);
+      g.events += __shfl_sync(0xffffffffu, ev, j);
+    }
+  }
+  timeout = __any_sync(0xffffffffu, timeout);
+  if (lane == 0) {
+    if (timeout) {
+      link_timeout(d.ctl);
+    } else if (ci.ok) {
+      Ctl c = load_ctl(d.ctl);
+      commit_tail(c, sp, g, ci, d.rec);
+      d.ctl->clipped = c.clipped;
+      d.ctl->events = c.events;
+      d.ctl->mass = c.mass;
+    }
+  }
+  return timeout ? 0 : 1;
 }
 
 // skip mask of tile u for the next step (blocks >= 1 of the finalize /

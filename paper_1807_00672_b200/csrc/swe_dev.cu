@@ -59,6 +59,11 @@ size_t arena_offset(long long C, int k) {
   return box + (size_t)k * arr;
 }
 
+// run loop choice by owned cells: the persistent kernel up to
+// here, the CUDA graph above.  (Linked parts too: the persistent kernel's
+// split exchange costs +1 us per step against the graph's +4.6 us at 1.28M
+// cells, but the 10M channel's measured-cost parts step slower on it:
+// 0.0845 vs 0.0768 ms at N = 8, profiles/r02_scaling_proxy_*.)
 constexpr int kPersistentMaxCells = 600000;
 
 int fail_invalid(const char* msg) {
@@ -617,10 +622,10 @@ int swe_dev_create(const swe_mesh_view* m, const swe_params* params, int device,
   if (const char* env = std::getenv("SWE_TILE_STAGE")) d.stage = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_DYN_TILES")) d.dyn = std::atoi(env) != 0;
   if (const char* env = std::getenv("SWE_GRAPH_UNROLL")) x->graph_unroll = std::max(1, std::atoi(env));
-  // run loop: the persistent kernel where a step's fixed cost matters (small
-  // meshes: 10k cells 7.9 vs 11.4 us per step), the CUDA graph of k_tile +
-  // k_finalize above (on par from ~1M cells on: 1M 31.7 vs 31.5 us, 10M
-  // 472 vs 470 us).  SWE_PERSISTENT=0/1 forces either.
+  // run loop: the persistent kernel where a step's fixed cost matters (10k
+  // cells 7.1 vs 11.4 us per step), the CUDA graph of k_tile + k_finalize
+  // above (1M 31.2 vs 31.5 us, 2.56M 129.3 vs 128.2, 10M 475 vs 460;
+  // DESIGN.md §4).  SWE_PERSISTENT=0/1 forces either.
   x->persistent = d.C_own <= kPersistentMaxCells;
   if (const char* env = std::getenv("SWE_PERSISTENT")) x->persistent = std::atoi(env) != 0;
   d.skip = 1;  // dry-tile skipping (fused kernel); SWE_NO_DRY_SKIP=1 turns it off

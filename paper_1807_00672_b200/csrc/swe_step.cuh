@@ -756,7 +756,8 @@ __device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
   Ctl& s_c = *reinterpret_cast<Ctl*>(base + kRunCtlOff + (sizeof(Dev) + 63) / 64 * 64);
   StepParams& s_sp = *reinterpret_cast<StepParams*>(base + kRunCtlOff + (sizeof(Dev) + 63) / 64 * 64 +
                                                     (sizeof(Ctl) + 63) / 64 * 64);
-  __shared__ int s_go;
+  __shared__ int s_go, s_tmo;
+  __shared__ double s_lo, s_hi;
   __shared__ CommitInfo s_ci;
   {
     const unsigned* src = reinterpret_cast<const unsigned*>(dg);
@@ -776,23 +777,55 @@ __device__ __noinline__ void run_control(const Dev* dg, Sync* sy, int nb) {
     const unsigned long long w0 = SWE_RUN_TIMING ? global_ns() : 0;
     const int par = (int)(s_c.step & 1);
     const Part* parts = d.part + (size_t)par * nb;
-    if (LINK) {  // the exchange carries every sum: reduce first, then post / wait / commit
+    if (LINK) {
+      // split exchange (swe_ctl.cuh): post the CFL bound / max speed (the
+      // workers' atomics) and the error slots at once, commit the head from
+      // the combined posts and publish it; then reduce and exchange the sums
+      unsigned long long c0 = 0, c1 = 0;
       if (threadIdx.x == 0) {
         poll_until(&sy->arrive, (unsigned)nb * (it + 1));
         fence_acq_rel_gpu();
+        if (SWE_RUN_TIMING) c0 = global_ns();
+        s_lo = __longlong_as_double((long long)__ldcg(&sy->lo[par]));
+        s_hi = __longlong_as_double((long long)__ldcg(&sy->hi[par]));
+        sy->lo[par] = 0x7ff0000000000000ULL;  // this parity's next use: two steps on
+        sy->hi[par] = 0ULL;
       }
       __syncthreads();
-      const Part p = reduce_parts_into(parts, nb, scratch);
       if (threadIdx.x < 32) {
-        post_outcome(d, p, 0);
-        wait_and_commit(d, 0, cudaGraphConditionalHandle{}, 0);
+        post_outcome(d, Part{s_lo, s_hi, 0.0, 0.0, 0, 0}, 0);
+        CommitInfo ci;
+        ci.ok = false;
+        bool tmo = false;
+        const int go = wait_commit_head(d, s_sp, ci, tmo);
+        if (threadIdx.x == 0) {
+          s_ci = ci;
+          s_go = go;
+          s_tmo = tmo;
+          s_c.step = __ldcg(&d.ctl->step);  // (the parity of the next step's slots)
+          const double t = __ldcg(&d.ctl->t), dts = __ldcg(&d.ctl->dts);
+          view_publish(&sy->view, it + 1, go, (t + dts >= s_sp.t_end) ? s_sp.t_end - t : dts);
+          if (SWE_RUN_TIMING) c1 = global_ns();
+        }
       }
       __syncthreads();
+      if (!s_tmo) {  // off the critical path: the sums in the fixed order, then across ranks
+        const Part p = reduce_parts_into(parts, nb, scratch);
+        if (threadIdx.x < 32) {
+          const CommitInfo ci = s_ci;
+          const int ok = post_wait_sums(d, s_sp, p, ci);
+          if (threadIdx.x == 0 && !ok && s_go) {  // stop the workers at their next view
+            s_go = 0;
+            view_publish(&sy->view, it + 2, 0, 0.0);
+          }
+        }
+        __syncthreads();
+      }
       if (threadIdx.x == 0) {
-        s_c.step = __ldcg(&d.ctl->step);
-        s_go = __ldcg(&d.ctl->active);
-        const double t = __ldcg(&d.ctl->t), dts = __ldcg(&d.ctl->dts);
-        view_publish(&sy->view, it + 1, s_go, (t + dts >= s_sp.t_end) ? s_sp.t_end - t : dts);
+        RUN_T(2, c0 - w0);
+        RUN_T(3, c1 - c0);
+        RUN_T(7, global_ns() - c1);
+        RUN_T(5, 1);
       }
       __syncthreads();
       if (!s_go) return;
@@ -1146,10 +1179,8 @@ __device__ __forceinline__ void run_body(const Dev& d, const Dev* dg, Sync* sy, 
         RUN_T(0, global_ns() - t_step);
         RUN_T(4, 1);
       }
-      if (!LINK) {
-        atomicMin(&sy->lo[par], (unsigned long long)__double_as_longlong(bp.lo));
-        atomicMax(&sy->hi[par], (unsigned long long)__double_as_longlong(bp.hi));
-      }
+      atomicMin(&sy->lo[par], (unsigned long long)__double_as_longlong(bp.lo));
+      atomicMax(&sy->hi[par], (unsigned long long)__double_as_longlong(bp.hi));
       atom_add_release_gpu(&sy->arrive, 1u);
     }
     // every worker has arrived: the next state and its dry-tile flags are

@@ -172,12 +172,14 @@ def test_cell_skip_pattern_matches_the_graph_loop():
 
 @pytest.mark.parametrize("name", ["three_mounds_friction", "channel"])
 def test_persistent_full_size_equals_graph_loop(name):
-    """Above kPersistentMaxCells the graph loop is the default; forced
-    persistent at full size (1.06M / 10.26M cells, 1183 workers, many tiles
-    per worker) is the same computation bit for bit."""
+    """Full size (1.06M / 10.26M cells, 1183 workers, many tiles per worker):
+    the persistent kernel and the graph loop are the same computation bit for
+    bit (the 10M mesh runs the graph loop by default)."""
     sc = api.make_scenario(name)
     m = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
-    a, b = solver(m, SWE_PERSISTENT=1), solver(m)
+    a, b = solver(m, SWE_PERSISTENT=1), solver(m, SWE_PERSISTENT=0)
+    if name == "channel":
+        assert solver(m).info()["persistent"] == 0
     assert a.info()["persistent"] == 1 and b.info()["persistent"] == 0
     out = []
     for s in (a, b):

@@ -22,13 +22,20 @@ ap.add_argument("--config", default="channel")
 ap.add_argument("--scale", type=float, default=1.0)
 ap.add_argument("--steps", type=int, default=200)
 ap.add_argument("--parts", type=int, default=1, help="time part 0 of an N-way RCB split")
+ap.add_argument("--part", type=int, default=0, help="which part of the split")
+ap.add_argument("--measured", action="store_true", help="measured-cost RCB (bench.py's split)")
+ap.add_argument("--self-link", action="store_true",
+                help="the whole mesh as ONE linked rank: the exchange's own cost per step")
 a = ap.parse_args()
 sc = api.make_scenario(a.config, scale=a.scale)
 m = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
-if a.parts > 1:
+if a.parts > 1 or a.self_link:
     from paper_1807_00672_b200 import dist
-    part = dist.partition(m, a.parts)
-    s = dist.LinkedPart(dist.local_mesh(m, part, 0))  # unlinked: its own dt
+    w = dist.measured_cost_weights(m, sc.state, parts=a.parts) if a.measured else None
+    part = dist.partition(m, a.parts, w)
+    s = dist.LinkedPart(dist.local_mesh(m, part, a.part))  # unlinked: its own dt
+    if a.self_link:
+        dist.link_local([s])
     s.stream = s.lib.swe_dev_stream(s.ctx)
     s.info = lambda: api.DeviceSolver.info(s)
     s.advance_async = lambda t_end, max_steps: s.launch(t_end=t_end, max_steps=max_steps)

@@ -1,9 +1,12 @@
 #!/usr/bin/env python3
 """Strong-scaling proxy on ONE GPU: split the 10M channel into N RCB parts,
-time each part's step (graph-launched, events) separately, and project the
-N-GPU step as max over parts (+ the measured cost of the linked exchange).
+time each part's step (events; the run loop the engine picks for the part)
+separately, and project the N-GPU step as max over parts (+ the measured
+cost of the linked exchange at the part's size: the channel scaled to 1/N,
+self-linked vs unlinked, on the run loop a linked rank of that size uses).
 Prints one JSON line."""
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -24,6 +27,29 @@ def time_part(lp, steps, torch):
     torch.cuda.synchronize()
     lp.records()
     return e0.elapsed_time(e1) / steps
+
+
+def exchange_cost(torch, api, dist, n, steps):
+    """ms per step that linking adds at 1/n of the channel (10.26M / n cells)"""
+    sc = api.make_scenario("channel", scale=(1.0 / n) ** 0.5)
+    mesh = api.build_mesh(sc.raw, sc.bed, sc.manning, device=0)
+    # a linked rank of this size: the persistent kernel up to 600k cells (swe_dev.cu)
+    old = os.environ.get("SWE_PERSISTENT")
+    os.environ["SWE_PERSISTENT"] = "1" if mesh.n_cells <= 600000 else "0"
+    try:
+        one = dist.LinkedPart(dist.local_mesh(mesh, dist.partition(mesh, 1), 0))
+    finally:
+        if old is None:
+            del os.environ["SWE_PERSISTENT"]
+        else:
+            os.environ["SWE_PERSISTENT"] = old
+    one.set_state(sc.state)
+    t0 = time_part(one, steps, torch)
+    dist.link_local([one])
+    one.set_state(sc.state)
+    t1 = time_part(one, steps, torch)
+    one.close()
+    return t1 - t0, mesh.n_cells, int(mesh.n_cells <= 600000)
 
 
 def weak(torch, api, dist, steps):
@@ -109,9 +135,11 @@ def main():
         if refine:
             out.setdefault("refine_history_ms_max", {})[n] = history
         mx = max(ts)
-        exch = t1l - t1
+        exch, exch_cells, exch_persistent = exchange_cost(torch, api, dist, n, steps)
         out[f"N{n}"] = {"ms_parts": ts, "owned_cells": cells, "wet_fraction": wet,
                         "ms_max": mx, "ms_mean": sum(ts) / n,
+                        "exchange_ms": exch, "exchange_measured_on_cells": exch_cells,
+                        "exchange_run_loop": "persistent" if exch_persistent else "graph",
                         "projected_efficiency_no_exchange": t1 / (n * mx),
                         "projected_efficiency": t1 / (n * (mx + exch))}
     print(json.dumps(out))
