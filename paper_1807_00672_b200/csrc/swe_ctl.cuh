@@ -183,6 +183,7 @@ struct Dev {
   int skip;
   int* dryflag;
   int* skipmask;
+  int2* streak;  // [ntiles] k_tile's consecutive skips (skip_code, swe_step.cuh)
   const int *nbr_off, *nbr;
   const int* soff;
   // persistent step kernel (k_run): barrier, double-buffered dry-tile flags

@@ -401,7 +401,9 @@ int build_tile_neighbours(swe_dev_ctx* x) {
   int* nbr = x->alloc<int>(std::max(1, nu));
   d.dryflag = x->alloc<int>(d.ntiles);
   d.skipmask = x->alloc<int>(d.ntiles);
+  d.streak = std::getenv("SWE_NO_HELD") ? nullptr : x->alloc<int2>(d.ntiles);
   if (!off || !nbr || !d.skipmask) return fail_invalid("dry-skip tables: cudaMalloc failed"), SWE_CUDA;
+  if (d.streak) CK(cudaMemsetAsync(d.streak, 0, sizeof(int2) * d.ntiles, s));
   k_pair_bounds<<<blocks_for(nu), kBlock, 0, s>>>(nu, k2, d.ntiles, off, nbr);
   CK(cudaMemsetAsync(d.dryflag, 0, sizeof(int) * d.ntiles, s));
   CK(cudaMemsetAsync(d.skipmask, 0, sizeof(int) * d.ntiles, s));
@@ -911,6 +913,7 @@ static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, con
     CK(cudaMemsetAsync(x->d.dryflag, 0, sizeof(int) * x->d.ntiles, s));
     CK(cudaMemsetAsync(x->d.skipmask, 0, sizeof(int) * x->d.ntiles, s));
   }
+  if (x->d.streak) CK(cudaMemsetAsync(x->d.streak, 0, sizeof(int2) * x->d.ntiles, s));
   if (x->d.pflag) CK(cudaMemsetAsync(x->d.pflag, 0, sizeof(int) * 2 * (size_t)x->d.ntiles, s));
   *x->h_ctl = c;
   CK(cudaMemcpyAsync(x->ctl, x->h_ctl, sizeof(Ctl), cudaMemcpyHostToDevice, s));
@@ -1433,6 +1436,7 @@ int swe_dev_link(swe_dev_ctx* x, int rank, int nranks, void* const* arenas,
     }
     x->h_ctl->cur = 0;
   }
+  if (d.streak) CK(cudaMemsetAsync(d.streak, 0, sizeof(int2) * d.ntiles, x->stream));
   x->h_ctl->xseq = 0;  // (a context is linked once; nothing has posted to it yet)
   x->h_ctl->cfl_valid = 0;
   x->cfl_host_valid = false;

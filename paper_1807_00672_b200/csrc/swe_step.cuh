@@ -370,6 +370,25 @@ __device__ __forceinline__ void tma_state(double* dst, int T, const double* H, c
 }
 #endif
 
+// Skip decision of tile tk for the step with tag `tag` (thread 0, kAhead
+// tiles ahead): 0 compute, 1 skip, 2 skip without writing the tile's next
+// state.  A tile that k_tile skipped at the two previous steps already holds
+// the state it would write in the next buffer: the step two back wrote
+// (h, 0, 0) there, and the step between copied the same h (skipped tiles keep
+// h bit for bit and zero q).  streak[tk] = {tag of its last skip by k_tile,
+// consecutive skips}; any other writer of the state (set_state, link, other
+// step kernels) breaks or clears the chain.
+__device__ __forceinline__ int skip_code(const Dev& d, int tk, int tag) {
+  if (tk >= d.ntiles) return 0;
+  const int m = __ldg(d.skipmask + tk);
+  const int2 st = d.streak ? d.streak[tk] : make_int2(0, 0);
+  if (m != tag) return 0;
+  if (!d.streak) return 1;
+  const bool chain = st.x == tag - 1;
+  d.streak[tk] = make_int2(tag, chain ? st.y + 1 : 1);
+  return chain && st.y >= 2 ? 2 : 1;
+}
+
 // LINK: linked context -- after the update, push the tile's cells that peers
 // hold as ghosts into the peers' next state buffers (see Link, swe_ctl.cuh).
 // (Finalizing in the kernel's last block instead of a separate launch was
@@ -431,7 +450,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   if (ahead && threadIdx.x == 0)
     for (int k = 0; k < kAhead; ++k) {
       const int tk = blockIdx.x + k * gridDim.x;
-      s_dec[k] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
+      s_dec[k] = skip_code(d, tk, tag);
     }
   __syncthreads();
   int it = 0;
@@ -449,7 +468,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (threadIdx.x == 0) {
         for (int k = 0; k < run; ++k) {
           const int tk = t + (kAhead + k) * gridDim.x;
-          s_dec[(it + kAhead + k) & 7] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
+          s_dec[(it + kAhead + k) & 7] = skip_code(d, tk, tag);
           d.dryflag[t + k * gridDim.x] = tag + 1;
         }
         atomicAdd(&ctl->skipped, (unsigned long long)run);
@@ -457,11 +476,14 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
         const int ck = (t + k * gridDim.x) * T;
         const int nk = min(T, d.C_own - ck);
+        const bool held = s_dec[(it + k) & 7] == 2;  // the next buffer holds it already
         for (int i = threadIdx.x; i < nk; i += NT) {
           const double h = H[ck + i];
-          NH[ck + i] = h;
-          NQX[ck + i] = 0.0;
-          NQY[ck + i] = 0.0;
+          if (!held) {
+            NH[ck + i] = h;
+            NQX[ck + i] = 0.0;
+            NQY[ck + i] = 0.0;
+          }
           a.mass += h * __ldg(d.area + ck + i);
         }
       }
@@ -530,7 +552,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (ahead) {
         sk = pre_skip;  // decided ahead; refill the ring
         const int tk = t + kAhead * gridDim.x;
-        s_dec[(it + kAhead) & 7] = tk < d.ntiles && __ldg(d.skipmask + tk) == tag;
+        s_dec[(it + kAhead) & 7] = skip_code(d, tk, tag);
       } else {
         sk = d.skip && __ldg(d.skipmask + t) == tag;
       }
