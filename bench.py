@@ -376,7 +376,7 @@ def run_b200_dist(args, rank, local, world):
     lp.set_state(sc.state)
     advance(W)
     steps = W
-    skipped0 = lp_skipped(lp)
+    skipped0, held0 = lp_skipped(lp), lp_held(lp)
     stream = torch.cuda.ExternalStream(dist_stream(lp), device=local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tdist.barrier()
@@ -395,9 +395,11 @@ def run_b200_dist(args, rank, local, world):
     ms = torch.tensor([ev0.elapsed_time(ev1)], device=dev)
     tdist.all_reduce(ms, op=tdist.ReduceOp.MAX)
     # dry tiles skipped over the timed steps, summed over ranks
-    sk = torch.tensor([float(lp_skipped(lp) - skipped0), float(lp_tiles(lp) * K)], device=dev)
+    sk = torch.tensor([float(lp_skipped(lp) - skipped0), float(lp_tiles(lp) * K),
+                       float(lp_held(lp) - held0)], device=dev)
     tdist.all_reduce(sk, op=tdist.ReduceOp.SUM)
     skip_frac = float(sk[0].item()) / max(1.0, float(sk[1].item()))
+    held_frac = float(sk[2].item()) / max(1.0, float(sk[1].item()))
     ms = float(ms.item())
     # e2e: host state in, the same K steps, owned state back to the host
     # (the state at step W -- the window's start -- is re-formed untimed)
@@ -446,7 +448,7 @@ def run_b200_dist(args, rank, local, world):
                                      "(k_tile with halo push, k_exchange); steps past the stop "
                                      "exit at once"),
                "clocks": clk.summary() if clk else None,
-               "roofline": dist_roofline(C, E, K, ms, world, skip_frac),
+               "roofline": dist_roofline(C, E, K, ms, world, skip_frac, held_frac),
                "e2e": {"value": C * K / float(e2e_s.item()), "unit": UNIT,
                        "h2d_bytes_per_step": 24 * C / K, "d2h_bytes_per_step": (24 * C + 40 * K) / K,
                        "path": "LinkedPart.set_state (host) + advance (K steps, records D2H) + "
@@ -531,13 +533,17 @@ def run_dist_host_driven(args, rank, local, world, sc, sizes, part, lm, setup_s,
 
 def _lp_info(lp):
     import ctypes
-    v = (ctypes.c_longlong * 12)()
-    lp.lib.swe_dev_info(lp.ctx, v, 12)
+    v = (ctypes.c_longlong * 16)()
+    lp.lib.swe_dev_info(lp.ctx, v, 16)
     return list(v)
 
 
 def lp_skipped(lp):
     return _lp_info(lp)[11]
+
+
+def lp_held(lp):
+    return _lp_info(lp)[15]
 
 
 def lp_tiles(lp):
@@ -558,17 +564,18 @@ def cfg_name(args):
     return "weak_square" if args.scaling == "weak" else args.config
 
 
-def dist_roofline(C, E, K, ms, world, skip_frac):
+def dist_roofline(C, E, K, ms, world, skip_frac, held_frac=0.0):
     """whole-job step roofline of an N-GPU run: SURVEY §8(d) canonical step
-    bytes (skipped dry tiles at 40 B/cell) over the max-over-ranks step time,
-    against N x the per-GPU HBM peak"""
+    bytes (skipped dry tiles at 40 B/cell, held ones at 16) over the
+    max-over-ranks step time, against N x the per-GPU HBM peak"""
     peak, src = load_peaks()
-    step = (1.0 - skip_frac) * (116 * C + 128 * E) + skip_frac * 40 * C
+    step = ((1.0 - skip_frac) * (116 * C + 128 * E) + (skip_frac - held_frac) * 40 * C
+            + held_frac * 16 * C)
     achieved = step / (ms / K / 1e3) / 1e9
     return {"bound": "hbm", "kernel": "step (all ranks)", "achieved": achieved,
             "peak": world * peak, "unit": "GB/s", "frac": achieved / (world * peak),
             "traffic": None, "peak_source": f"{world} x {src}",
-            "skipped_tile_fraction": skip_frac}
+            "skipped_tile_fraction": skip_frac, "held_tile_fraction": held_frac}
 
 
 def dist_stream(part_solver):
@@ -615,7 +622,8 @@ def run_b200(args):
     solver.advance(t_end=horizon, max_steps=W)
     _, step0 = solver.clock()
     assert step0 == W
-    skipped0 = solver.info()["skipped_tiles"]
+    inf_0 = solver.info()
+    skipped0, held0 = inf_0["skipped_tiles"], inf_0["held_tiles"]
     # e2e replays the same K steps from this state (untimed copy-out here)
     e2e_start = None if args.no_e2e else solver.get_state()
 
@@ -635,6 +643,7 @@ def run_b200(args):
     clk.stop()
     info0 = solver.info()
     skip_frac = (info0["skipped_tiles"] - skipped0) / max(1, K * info0["tiles"])
+    held_frac = (info0["held_tiles"] - held0) / max(1, K * info0["tiles"])
     launches = api.launch_count() - launches0
     assert len(recs) == K, f"expected {K} steps, ran {len(recs)}"
     ms = ev0.elapsed_time(ev1)
@@ -649,7 +658,8 @@ def run_b200(args):
     # plain launches with events per kernel on the solver's stream
     solver.set_state(sc.state)
     solver.advance(t_end=horizon, max_steps=W)
-    skipped1 = solver.info()["skipped_tiles"]
+    inf_1 = solver.info()
+    skipped1, held1 = inf_1["skipped_tiles"], inf_1["held_tiles"]
     solver.set_profiling(True)
     solver.advance_n_async(K, t_end=horizon)
     solver.synchronize()
@@ -657,11 +667,14 @@ def run_b200(args):
     solver.set_profiling(False)
     info = solver.info()
     prof_skip = (info["skipped_tiles"] - skipped1) / max(1, K * info["tiles"])
+    prof_held = (info["held_tiles"] - held1) / max(1, K * info["tiles"])
     avg = lambda k: kt[k][0] / max(1, kt[k][1])  # noqa: E731
     fin_ms = avg("finalize")
     peak, peak_src = load_peaks()
     step_bytes = 116 * C + 128 * E  # SURVEY.md §8(d) canonical B_step
-    step_eff = (1.0 - skip_frac) * step_bytes + skip_frac * 40 * C  # skipped tiles: 40 B/cell
+    # skipped tiles: 40 B/cell (h, area in; state out), held ones 16 B/cell (h, area in)
+    step_eff = ((1.0 - skip_frac) * step_bytes + (skip_frac - held_frac) * 40 * C
+                + held_frac * 16 * C)
     prof = load_traffic()
     if prof.get("config", "channel") != args.config or args.scale != 1.0:
         prof = {}  # the committed capture is of another mesh: no per-launch bytes for this one
@@ -672,8 +685,9 @@ def run_b200(args):
         tile_ms = avg("tile")
         kernels = {"tile": tile_ms, "finalize": fin_ms}
         own = 80 * C + 32 * E + 4 * info["halo_edges"]  # the fused kernel's own compulsory bytes
-        dom = ("tile", tile_ms, (1.0 - prof_skip) * step_bytes + prof_skip * 40 * C,
-               (1.0 - prof_skip) * own + prof_skip * 40 * C)
+        skipped_b = (prof_skip - prof_held) * 40 * C + prof_held * 16 * C
+        dom = ("tile", tile_ms, (1.0 - prof_skip) * step_bytes + skipped_b,
+               (1.0 - prof_skip) * own + skipped_b)
     else:
         face_ms, cell_ms = avg("face"), avg("cell")
         kernels = {"face": face_ms, "cell": cell_ms, "finalize": fin_ms}
@@ -690,7 +704,8 @@ def run_b200(args):
             "canonical_frac": achieved / peak,
             "canonical_bytes_per_launch": dom[2],
             "canonical_note": "SURVEY.md 8(d) B_step = 116 C + 128 E per step (one k_tile "
-                              "launch), dry tiles skipped in this window counted at 40 B/cell",
+                              "launch), dry tiles skipped in this window counted at 40 B/cell, "
+                              "held ones (next state already in place, no writes) at 16 B/cell",
             "dram_frac": (traffic / t_s / 1e9 / peak) if traffic else None,
             "dram_note": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one launch "
                          "(committed capture, profiles/traffic.json) over this run's mean launch "
@@ -735,6 +750,7 @@ def run_b200(args):
                  if info["dry_skip"] else ms / K)
         out["dry_tile_skip"] = {
             "enabled": bool(info["dry_skip"]), "skipped_tile_fraction": skip_frac,
+            "held_tile_fraction": held_frac,
             "note": "tiles whose cells and ring were dry and at rest after the previous step "
                     "are updated without evaluating their edges (every mass flux is exactly "
                     "+-0, the clamp zeroes q); results bit-identical (tests/test_gpu_parity.py)",

@@ -250,7 +250,8 @@ SWE_API int swe_dev_kernel_times(swe_dev_ctx* ctx, double* ms, long long* launch
  * [8] tile shared-memory bytes, [9] edges, [10] dry-tile skipping on?,
  * [11] dry tiles skipped so far (n > 11 synchronises the context),
  * [12] steps per WHILE iteration of the run graph, [13] run loop is the
- * persistent kernel?, [14] its CTAs. */
+ * persistent kernel?, [14] its CTAs, [15] of the skipped tiles, those whose
+ * next state was already in place (no writes). */
 SWE_API int swe_dev_info(swe_dev_ctx* ctx, long long* out, int n);
 
 /* Per cell (reference numbering): 1 if dry-tile skipping will skip the cell's

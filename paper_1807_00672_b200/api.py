@@ -610,11 +610,11 @@ class DeviceSolver:
         return {k: (ms[i], n[i]) for i, k in enumerate(names)}
 
     def info(self) -> dict:
-        v = (C.c_longlong * 15)()
-        _check(self.lib.swe_dev_info(self.ctx, v, 15), "swe_dev_info")
+        v = (C.c_longlong * 16)()
+        _check(self.lib.swe_dev_info(self.ctx, v, 16), "swe_dev_info")
         keys = ("fused", "tile_cells", "tiles", "max_slots", "halo_edges", "grid_tile",
                 "grid_face", "grid_cell", "tile_smem_bytes", "edges", "dry_skip",
-                "skipped_tiles", "graph_unroll", "persistent", "grid_run")
+                "skipped_tiles", "graph_unroll", "persistent", "grid_run", "held_tiles")
         return dict(zip(keys, list(v)))
 
     @property

@@ -54,6 +54,7 @@ struct Ctl {
   unsigned int done;        // blocks of the running step kernel that finished
   int tile_next;            // dynamic tile counter of k_tile (reset by finalize)
   unsigned long long skipped;  // dry tiles skipped by k_tile (cumulative)
+  unsigned long long held;     // ... of which held: next state already in place, no writes
 };
 
 struct Part {  // one block's partial results

@@ -1288,11 +1288,12 @@ int swe_dev_info(swe_dev_ctx* x, long long* out, int n) {
   if (!x || !out) return fail_invalid("null argument");
   if (n > 11)
     if (int rc = sync_ctl(x)) return rc;
-  const long long v[15] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
+  const long long v[16] = {x->fused ? 1 : 0, x->d.T, x->d.ntiles, x->max_slots, x->n_halo,
                            x->grid_tile, x->grid_face, x->grid_cell, (long long)x->tile_smem,
                            x->d.E, x->d.skip, n > 11 ? (long long)x->h_ctl->skipped : 0,
-                           x->graph_unroll, x->persistent ? 1 : 0, x->grid_run};
-  for (int i = 0; i < n && i < 15; ++i) out[i] = v[i];
+                           x->graph_unroll, x->persistent ? 1 : 0, x->grid_run,
+                           n > 15 ? (long long)x->h_ctl->held : 0};
+  for (int i = 0; i < n && i < 16; ++i) out[i] = v[i];
   return SWE_OK;
 }
 

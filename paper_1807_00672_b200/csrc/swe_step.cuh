@@ -466,12 +466,15 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       int run = 1;
       while (run < kAhead && s_dec[(it + run) & 7]) ++run;
       if (threadIdx.x == 0) {
+        int held = 0;
         for (int k = 0; k < run; ++k) {
+          held += s_dec[(it + k) & 7] == 2;
           const int tk = t + (kAhead + k) * gridDim.x;
           s_dec[(it + kAhead + k) & 7] = skip_code(d, tk, tag);
           d.dryflag[t + k * gridDim.x] = tag + 1;
         }
         atomicAdd(&ctl->skipped, (unsigned long long)run);
+        if (held) atomicAdd(&ctl->held, (unsigned long long)held);
       }
       for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
         const int ck = (t + k * gridDim.x) * T;
