@@ -438,7 +438,7 @@ __global__ void __launch_bounds__(kBlock) k_prepare(Dev d, int n) {
 __global__ void k_set_params(StepParams* sp, StepParams v) { *sp = v; }
 
 // gate: opens a launch sequence (run() loop entry, engine.hpp:355-358)
-__global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
+__device__ __forceinline__ void gate(const Dev& d, cudaGraphConditionalHandle cond, int use_cond) {
   Ctl* c = d.ctl;
   StepParams* sp = const_cast<StepParams*>(d.sp);
   if (sp->add_steps > 0) {
@@ -473,6 +473,16 @@ __global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
   }
   c->active = go;
   if (use_cond) cudaGraphSetConditional(cond, go);
+}
+
+__global__ void k_gate(Dev d, cudaGraphConditionalHandle cond, int use_cond) {
+  gate(d, cond, use_cond);
+}
+
+// the step parameters and the gate in one launch (the persistent loop's prologue)
+__global__ void k_gate_params(Dev d, StepParams v) {
+  *const_cast<StepParams*>(d.sp) = v;
+  gate(d, cudaGraphConditionalHandle{}, 0);
 }
 
 // Ctl through L2 (ld.cg): a step kernel's last block reads fields other

@@ -103,6 +103,8 @@ struct swe_dev_ctx {
   int graph_unroll = 8;         // steps per WHILE iteration of the graph (SWE_GRAPH_UNROLL)
   bool persistent = false;      // run loop = one cooperative k_run launch (SWE_PERSISTENT=0: graph)
   Dev* d_dev = nullptr;         // device copy of d for k_run's commit path
+  Dev d_dev_host{};             // what d_dev holds
+  bool d_dev_valid = false;
   int grid_run = 0;             // CTAs of k_run (= grid_tile when the occupancies agree)
   std::vector<void*> link_allocs;  // device tables of the link
   std::vector<void*> ipc_mapped;   // peers' arenas opened through CUDA IPC
@@ -222,11 +224,20 @@ const void* run_kernel(int threads, bool link) {
   return link ? (const void*)k_run<256, true> : (const void*)k_run<256, false>;
 }
 
-// the run loop as one cooperative launch of the persistent step kernel
-int launch_run(swe_dev_ctx* x) {
+// the run loop as one cooperative launch of the persistent step kernel,
+// after its prologue (step parameters + gate in one launch)
+int launch_run(swe_dev_ctx* x, const StepParams& v) {
+  k_gate_params<<<1, 1, 0, x->stream>>>(x->d, v);
+  ++g_launches;
+  CK(cudaGetLastError());
   Dev dcopy = x->d;
-  // the commit path reads the context's Dev from global memory (stream-ordered copy)
-  CK(cudaMemcpyAsync(x->d_dev, &x->d, sizeof(Dev), cudaMemcpyHostToDevice, x->stream));
+  // the commit path reads the context's Dev from global memory (stream-ordered
+  // copy, only when it changed: a pageable copy costs ~10 us per launch)
+  if (!x->d_dev_valid || std::memcmp(&x->d_dev_host, &x->d, sizeof(Dev)) != 0) {
+    CK(cudaMemcpyAsync(x->d_dev, &x->d, sizeof(Dev), cudaMemcpyHostToDevice, x->stream));
+    x->d_dev_host = x->d;
+    x->d_dev_valid = true;
+  }
   const Dev* dg = x->d_dev;
   void* args[] = {&dcopy, &dg};
   CK(cudaLaunchCooperativeKernel(run_kernel(x->tile_threads, x->linked), dim3(x->grid_run),
@@ -264,6 +275,19 @@ int ensure_cfl(swe_dev_ctx* x, bool force = false) {
 
 // step parameters travel as a kernel argument (captured at launch: no
 // host buffer to race with when launches are only enqueued)
+StepParams make_params(double t_end, long long max_steps, double next_snap, long long rec_cap,
+                       int ring, int mode = 0, long long add_steps = 0) {
+  StepParams v;
+  v.add_steps = add_steps;
+  v.t_end = t_end;
+  v.max_steps = max_steps;
+  v.next_snap = next_snap;
+  v.rec_cap = rec_cap;
+  v.ring = ring;
+  v.mode = mode;
+  return v;
+}
+
 int write_params(swe_dev_ctx* x, double t_end, long long max_steps, double next_snap,
                  long long rec_cap, int ring, int mode = 0, long long add_steps = 0) {
   StepParams v;
@@ -1024,15 +1048,15 @@ int swe_dev_advance(swe_dev_ctx* x, double t_end, long long max_steps, double ne
   if (n_done) *n_done = 0;
   const long long cap = std::min<long long>(max_records > 0 ? max_records : x->rec_cap, x->rec_cap);
   if (int rc = ensure_cfl(x)) return rc;
-  if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
   if (x->persistent) {
-    if (int rc = launch_gate(x)) return rc;
-    if (int rc = launch_run(x)) return rc;
+    if (int rc = launch_run(x, make_params(t_end, max_steps, next_snap, cap, 0))) return rc;
   } else if (x->exec) {
+    if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
     CK(cudaGraphLaunch(x->exec, x->stream));
     ++g_launches;
   } else {
     // no graph: step until the device says stop (checked every 64 steps)
+    if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
     if (int rc = launch_gate(x)) return rc;
     for (long long k = 0; k < cap; ++k) {
       if (int rc = plain_step(x, 0)) return rc;
@@ -1058,11 +1082,8 @@ int swe_dev_advance_async(swe_dev_ctx* x, double t_end, long long max_steps, dou
     return fail_invalid("swe_dev_advance_async: context was created without a graph");
   const long long cap = std::min<long long>(max_records > 0 ? max_records : x->rec_cap, x->rec_cap);
   if (int rc = ensure_cfl(x)) return rc;
+  if (x->persistent) return launch_run(x, make_params(t_end, max_steps, next_snap, cap, 0));
   if (int rc = write_params(x, t_end, max_steps, next_snap, cap, 0)) return rc;
-  if (x->persistent) {
-    if (int rc = launch_gate(x)) return rc;
-    return launch_run(x);
-  }
   CK(cudaGraphLaunch(x->exec, x->stream));
   ++g_launches;
   return SWE_OK;
@@ -1083,11 +1104,8 @@ int swe_dev_records(swe_dev_ctx* x, swe_step_record* series, long long max_recor
 int swe_dev_advance_n_async(swe_dev_ctx* x, long long n, double t_end) {
   if (!x) return fail_invalid("null context");
   if (int rc = ensure_cfl(x)) return rc;
-  if (!x->profiling && x->persistent) {  // exactly n steps: the gate sets max_steps = step + n
-    if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, x->rec_cap, 1, 0, n)) return rc;
-    if (int rc = launch_gate(x)) return rc;
-    return launch_run(x);
-  }
+  if (!x->profiling && x->persistent)  // exactly n steps: the gate sets max_steps = step + n
+    return launch_run(x, make_params(t_end, LLONG_MAX, INFINITY, x->rec_cap, 1, 0, n));
   if (int rc = write_params(x, t_end, LLONG_MAX, INFINITY, x->rec_cap, 1)) return rc;
   if (int rc = launch_gate(x)) return rc;
   if (x->profiling) {
