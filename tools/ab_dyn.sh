@@ -1,4 +1,5 @@
 #!/bin/bash
+# (record of a reverted experiment: the switch it sets no longer exists; DESIGN.md §4 / §9)
 # A/B of the persistent kernel's tile schedule: round robin vs dynamic (SWE_RUN_DYN=1), and the graph loop
 out=gpurun_out/r02_ab_dyn.txt
 : > $out

@@ -1,4 +1,5 @@
 #!/bin/bash
+# (record of a reverted experiment: the switch it sets no longer exists; DESIGN.md §4 / §9)
 # persistent kernel: longest poll back-off (SWE_POLL_CAP ns)
 out=gpurun_out/r02_ab_poll.txt
 : > $out
