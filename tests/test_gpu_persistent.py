@@ -192,3 +192,23 @@ def test_persistent_full_size_equals_graph_loop(name):
     assert bit_equal(ra, rb) and la == lb
     for k in ("h", "qx", "qy"):
         assert bit_equal(getattr(sa, k), getattr(sb, k)), k
+
+
+@pytest.mark.timeout(120)
+def test_linked_step_exchange_timeout_stops_the_persistent_kernel():
+    """A peer that stops posting mid-run: the control CTA's wait for the step
+    outcome (split exchange, swe_ctl.cuh wait_commit_head) times out, the
+    workers see a stop in the published view, and the run ends with an error
+    instead of a hang."""
+    sc = api.make_scenario("sloping_wet_dry", scale=0.03)
+    m = api.build_mesh(sc.raw, sc.bed, sc.manning)
+    part = dist.partition(m, 2)
+    parts = [dist.LinkedPart(dist.local_mesh(m, part, p)) for p in range(2)]
+    assert all(api.DeviceSolver.info(p)["persistent"] == 1 for p in parts)
+    dist.link_local(parts, timeout_s=0.5)
+    for p in parts:
+        p.set_state(sc.state)
+    recs = dist.run_ranks(parts, 6)  # both ranks: the CFL cache is formed, 6 steps
+    assert len(recs) == 6
+    with pytest.raises(api.DeviceError):
+        parts[0].advance(max_steps=int(recs[-1, 0]) + 4)  # rank 1 never posts again
