@@ -112,6 +112,9 @@ struct swe_dev_ctx {
   double* snap[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t snap_ready[2] = {nullptr, nullptr}, snap_done[2] = {nullptr, nullptr};
+  // state transfers: one event per array + one for the main stream's position
+  cudaStream_t xfer_stream = nullptr;
+  cudaEvent_t xfer_ev[4] = {nullptr, nullptr, nullptr, nullptr};
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
@@ -901,6 +904,9 @@ int swe_dev_destroy(swe_dev_ctx* x) {
     if (x->snap_done[i]) cudaEventDestroy(x->snap_done[i]);
   }
   if (x->copy_stream) cudaStreamDestroy(x->copy_stream);
+  if (x->xfer_stream) cudaStreamSynchronize(x->xfer_stream), cudaStreamDestroy(x->xfer_stream);
+  for (cudaEvent_t e : x->xfer_ev)
+    if (e) cudaEventDestroy(e);
   cudaFree(x->halo_send);
   cudaFree(x->halo_recv);
   if (x->h_ctl) cudaFreeHost(x->h_ctl);
@@ -909,21 +915,39 @@ int swe_dev_destroy(swe_dev_ctx* x) {
   return SWE_OK;
 }
 
+// the state transfers' own stream and events (created on first use)
+static int ensure_xfer(swe_dev_ctx* x) {
+  if (x->xfer_stream) return SWE_OK;
+  CK(cudaStreamCreateWithFlags(&x->xfer_stream, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : x->xfer_ev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return SWE_OK;
+}
+
+// Host state in: each array's copy runs on the transfer stream while the
+// previous array is permuted into device order on the main stream (one array
+// per gather: its 82 MB source at 10M cells stays in L2 for the random reads)
 static int set_state_impl(swe_dev_ctx* x, const double* h, const double* qx, const double* qy,
                           double t, long long step, cudaMemcpyKind kind) {
   if (!x || !h || !qx || !qy) return fail_invalid("swe_dev_set_state: null argument");
   const int C = x->d.C;
   cudaStream_t s = x->stream;
+  CK(cudaSetDevice(x->device));
   if (int rc = sync_ctl(x)) return rc;
+  if (int rc = ensure_xfer(x)) return rc;
   Ctl c = *x->h_ctl;
-  CK(cudaMemcpyAsync(x->stage_h, h, sizeof(double) * C, kind, s));
-  CK(cudaMemcpyAsync(x->stage_qx, qx, sizeof(double) * C, kind, s));
-  CK(cudaMemcpyAsync(x->stage_qy, qy, sizeof(double) * C, kind, s));
-  k_state_in<<<blocks_for(C), kBlock, 0, s>>>(C, x->d.c_orig, x->stage_h, x->stage_qx,
-                                               x->stage_qy, x->d.h[c.cur], x->d.qx[c.cur],
-                                               x->d.qy[c.cur]);
-  ++g_launches;
-  CK(cudaGetLastError());
+  const double* src[3] = {h, qx, qy};
+  double* stg[3] = {x->stage_h, x->stage_qx, x->stage_qy};
+  double* dst[3] = {x->d.h[c.cur], x->d.qx[c.cur], x->d.qy[c.cur]};
+  CK(cudaEventRecord(x->xfer_ev[3], s));  // the staging buffers are free from here
+  CK(cudaStreamWaitEvent(x->xfer_stream, x->xfer_ev[3], 0));
+  for (int k = 0; k < 3; ++k) {
+    CK(cudaMemcpyAsync(stg[k], src[k], sizeof(double) * C, kind, x->xfer_stream));
+    CK(cudaEventRecord(x->xfer_ev[k], x->xfer_stream));
+    CK(cudaStreamWaitEvent(s, x->xfer_ev[k], 0));
+    k_gather<double><<<blocks_for(C), kBlock, 0, s>>>(C, x->d.c_orig, stg[k], dst[k]);
+    ++g_launches;
+    CK(cudaGetLastError());
+  }
   c.t = t;
   c.step = step;
   c.cfl_valid = 0;
@@ -965,15 +989,23 @@ static int get_state_impl(swe_dev_ctx* x, double* h, double* qx, double* qy, dou
   if (t) *t = x->h_ctl->t;
   if (step) *step = x->h_ctl->step;
   if (!h && !qx && !qy) return SWE_OK;
-  k_state_out<<<blocks_for(C), kBlock, 0, s>>>(C, x->d.c_new, x->d.h[cur], x->d.qx[cur],
-                                                x->d.qy[cur], x->stage_h, x->stage_qx,
-                                                x->stage_qy);
-  ++g_launches;
-  CK(cudaGetLastError());
-  if (h) CK(cudaMemcpyAsync(h, x->stage_h, sizeof(double) * C, kind, s));
-  if (qx) CK(cudaMemcpyAsync(qx, x->stage_qx, sizeof(double) * C, kind, s));
-  if (qy) CK(cudaMemcpyAsync(qy, x->stage_qy, sizeof(double) * C, kind, s));
-  CK(cudaStreamSynchronize(s));
+  CK(cudaSetDevice(x->device));
+  if (int rc = ensure_xfer(x)) return rc;
+  // each array permuted to reference order on the main stream, then copied
+  // out on the transfer stream while the next one is permuted
+  double* out[3] = {h, qx, qy};
+  const double* dev[3] = {x->d.h[cur], x->d.qx[cur], x->d.qy[cur]};
+  double* stg[3] = {x->stage_h, x->stage_qx, x->stage_qy};
+  for (int k = 0; k < 3; ++k) {
+    if (!out[k]) continue;
+    k_gather<double><<<blocks_for(C), kBlock, 0, s>>>(C, x->d.c_new, dev[k], stg[k]);
+    ++g_launches;
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(x->xfer_ev[k], s));
+    CK(cudaStreamWaitEvent(x->xfer_stream, x->xfer_ev[k], 0));
+    CK(cudaMemcpyAsync(out[k], stg[k], sizeof(double) * C, kind, x->xfer_stream));
+  }
+  CK(cudaStreamSynchronize(x->xfer_stream));
   return SWE_OK;
 }
 
