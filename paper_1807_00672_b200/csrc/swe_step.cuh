@@ -438,8 +438,12 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
   const Phys P = d.P;
   CellAcc a{INFINITY, 0.0, 0.0, 0.0, 0};
 
-  constexpr int kAhead = 4;  // skip decisions known ahead per CTA (ring s_dec[8])
-  __shared__ int s_next, s_skip, s_dec[8];
+#ifndef SWE_SKIP_AHEAD
+#define SWE_SKIP_AHEAD 4
+#endif
+  constexpr int kAhead = SWE_SKIP_AHEAD;  // skip decisions known ahead per CTA (ring s_dec)
+  constexpr int kRing = 2 * kAhead, kMask = kRing - 1;
+  __shared__ int s_next, s_skip, s_dec[kRing];
   // dry-tile skipping: skipmask[t] == tag(state) <=> tile t and its ring were
   // dry and at rest (computed by the finalize launch from the flags this
   // kernel writes, tagged with the step of the state they describe).  With
@@ -458,19 +462,19 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
     const int c0 = t * T;
     SWE_CHECK(t >= 0 && t < d.ntiles && c0 < d.C_own);
     const int nc = min(T, d.C_own - c0);
-    const bool pre_skip = ahead && s_dec[it & 7] != 0;
+    const bool pre_skip = ahead && s_dec[it & kMask] != 0;
     if (pre_skip) {
       // skipped tiles, fast path: a run of up to kAhead consecutive skipped
       // tiles of this CTA in one round trip, no shared memory (a tile with
       // halo pushes is never in the skip mask)
       int run = 1;
-      while (run < kAhead && s_dec[(it + run) & 7]) ++run;
+      while (run < kAhead && s_dec[(it + run) & kMask]) ++run;
       if (threadIdx.x == 0) {
         int held = 0;
         for (int k = 0; k < run; ++k) {
-          held += s_dec[(it + k) & 7] == 2;
+          held += s_dec[(it + k) & kMask] == 2;
           const int tk = t + (kAhead + k) * gridDim.x;
-          s_dec[(it + kAhead + k) & 7] = skip_code(d, tk, tag);
+          s_dec[(it + kAhead + k) & kMask] = skip_code(d, tk, tag);
           d.dryflag[t + k * gridDim.x] = tag + 1;
         }
         atomicAdd(&ctl->skipped, (unsigned long long)run);
@@ -479,7 +483,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
         const int ck = (t + k * gridDim.x) * T;
         const int nk = min(T, d.C_own - ck);
-        const bool held = s_dec[(it + k) & 7] == 2;  // the next buffer holds it already
+        const bool held = s_dec[(it + k) & kMask] == 2;  // the next buffer holds it already
         for (int i = threadIdx.x; i < nk; i += NT) {
           const double h = H[ck + i];
           if (!held) {
@@ -510,7 +514,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       const int tn = t + gridDim.x;
       pf_tile = -1;
       if (SWE_TILE_TMA == 1 && tn < d.ntiles && (tn + 1) * T <= d.C_own &&
-          !(ahead && s_dec[(it + 1) & 7])) {
+          !(ahead && s_dec[(it + 1) & kMask])) {
         if (threadIdx.x == 0)
           tma_state(tbuf + (cb ^ 1) * 3 * T, T, H, QX, QY, tn * T, (unsigned)(T * sizeof(double)),
                     &s_bar[cb ^ 1]);
@@ -555,7 +559,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
       if (ahead) {
         sk = pre_skip;  // decided ahead; refill the ring
         const int tk = t + kAhead * gridDim.x;
-        s_dec[(it + kAhead) & 7] = skip_code(d, tk, tag);
+        s_dec[(it + kAhead) & kMask] = skip_code(d, tk, tag);
       } else {
         sk = d.skip && __ldg(d.skipmask + t) == tag;
       }
