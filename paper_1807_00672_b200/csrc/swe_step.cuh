@@ -480,18 +480,58 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
         atomicAdd(&ctl->skipped, (unsigned long long)run);
         if (held) atomicAdd(&ctl->held, (unsigned long long)held);
       }
-      for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
-        const int ck = (t + k * gridDim.x) * T;
-        const int nk = min(T, d.C_own - ck);
-        const bool held = s_dec[(it + k) & kMask] == 2;  // the next buffer holds it already
-        for (int i = threadIdx.x; i < nk; i += NT) {
-          const double h = H[ck + i];
-          if (!held) {
-            NH[ck + i] = h;
-            NQX[ck + i] = 0.0;
-            NQY[ck + i] = 0.0;
+#ifndef SWE_SKIP_HOIST
+#define SWE_SKIP_HOIST 1
+#endif
+      if (SWE_SKIP_HOIST && T <= 2 * NT) {
+        // every load of the run first (up to kAhead tiles x 2 cells per
+        // thread), then the stores and the mass in tile, cell order: one
+        // round trip for the run instead of one per cell
+        double hv[kAhead][2], av[kAhead][2];
+#pragma unroll
+        for (int k = 0; k < kAhead; ++k) {
+          const int ck = (t + k * gridDim.x) * T;
+          const int nk = k < run ? min(T, d.C_own - ck) : 0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = threadIdx.x + j * NT;
+            hv[k][j] = i < nk ? H[ck + i] : 0.0;
+            av[k][j] = i < nk ? __ldg(d.area + ck + i) : 0.0;
           }
-          a.mass += h * __ldg(d.area + ck + i);
+        }
+#pragma unroll
+        for (int k = 0; k < kAhead; ++k) {
+          if (k >= run) break;
+          const int ck = (t + k * gridDim.x) * T;
+          const int nk = min(T, d.C_own - ck);
+          const bool held = s_dec[(it + k) & kMask] == 2;  // the next buffer holds it already
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const int i = threadIdx.x + j * NT;
+            if (i < nk) {
+              if (!held) {
+                NH[ck + i] = hv[k][j];
+                NQX[ck + i] = 0.0;
+                NQY[ck + i] = 0.0;
+              }
+              a.mass += hv[k][j] * av[k][j];
+            }
+          }
+        }
+      } else {
+        for (int k = 0; k < run; ++k) {  // tile order, then cell order: the mass sums' order
+          const int ck = (t + k * gridDim.x) * T;
+          const int nk = min(T, d.C_own - ck);
+          const bool held = s_dec[(it + k) & kMask] == 2;  // the next buffer holds it already
+          for (int i = threadIdx.x; i < nk; i += NT) {
+            const double h = H[ck + i];
+            if (!held) {
+              NH[ck + i] = h;
+              NQX[ck + i] = 0.0;
+              NQY[ck + i] = 0.0;
+            }
+            a.mass += h * __ldg(d.area + ck + i);
+          }
         }
       }
       __syncthreads();  // s_dec refill
