@@ -443,6 +443,7 @@ __global__ void __launch_bounds__(NT, SWE_TILE_BLOCKS(NT)) k_tile(Dev d) {
 #endif
   constexpr int kAhead = SWE_SKIP_AHEAD;  // skip decisions known ahead per CTA (ring s_dec)
   constexpr int kRing = 2 * kAhead, kMask = kRing - 1;
+  static_assert((kAhead & (kAhead - 1)) == 0 && kAhead <= 16, "SWE_SKIP_AHEAD: a power of two");
   __shared__ int s_next, s_skip, s_dec[kRing];
   // dry-tile skipping: skipmask[t] == tag(state) <=> tile t and its ring were
   // dry and at rest (computed by the finalize launch from the flags this
