@@ -715,6 +715,14 @@ def run_b200(args):
                           "capture over the mean launch time, against the measured DFMA peak "
                           f"{fpk['dfma_per_s']:.3e}/s (profiles/r02_fp64_peak.json)") if fpk else
                          "no FP64 peak measured",
+            # issue roofline: warp-instructions per launch (ncu capture) over the
+            # SMs' issue capacity (4 schedulers x 1 warp-instruction per clock)
+            "issue_frac": ((prof[dom[0] + "_warp_inst"] / t_s)
+                           / (4 * fpk["sms"] * fpk["clock_mhz_attr"] * 1e6))
+                          if (fpk and prof.get(dom[0] + "_warp_inst")) else None,
+            "issue_note": "smsp__inst_executed.sum per launch (profiles/traffic.json) over the mean "
+                          "launch time, against 4 warp-instructions per SM per clock at the "
+                          "attribute clock (profiles/r02_fp64_peak.json sms, clock_mhz_attr)",
             "own_bytes_per_launch": dom[3],
             "own_frac": dom[3] / t_s / 1e9 / peak,
             "limiter": prof.get(dom[0] + "_limiter"),
