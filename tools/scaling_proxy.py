@@ -107,8 +107,8 @@ def main():
         weights = dist.cost_weights(sc.state, mesh=mesh)
         out["partition"] = "cost-weighted RCB (wet/dry model)"
     if "--measured" in sys.argv:
-        cc = float(sys.argv[sys.argv.index("--measured") + 1]) \
-            if len(sys.argv) > sys.argv.index("--measured") + 1 else None
+        nxt = sys.argv[sys.argv.index("--measured") + 1:][:1]
+        cc = float(nxt[0]) if nxt and not nxt[0].startswith("--") else None
         out["partition"] = f"cost-weighted RCB (measured skip pattern, computed tiles {cc}x)"
     refine = int(sys.argv[sys.argv.index("--refine") + 1]) if "--refine" in sys.argv else 0
     for n in (2, 4, 8):
