@@ -67,3 +67,34 @@ def test_reference_arm_runs_the_reference_only():
                                                 d["config"]["boundary_edges"], 1)
     assert d["cpu_baseline"]["host"]["hardware_concurrency"] >= 1
     assert "steps [3, 6)" in d["cpu_baseline"]["sample"]
+
+
+@pytest.mark.gpu
+def test_b200_arm_line_carries_the_contract():
+    """The B200 arm's JSON line on config [0]: the base keys, roofline with its
+    measured peak, cpu_baseline (parallel + one-thread legs), e2e with the
+    copies' bytes, clocks sampled in the timed region, gpu_launches, and the
+    same config dict as the reference arm."""
+    sys.path.insert(0, str(ROOT))
+    import bench
+    d = run_bench("--config", "circular_dam_break", "--steps", "20", "--warmup", "3",
+                  "--cpu-seconds", "2")
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+              "higher_is_better", "scaling", "vs_baseline", "dtype", "data", "config",
+              "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert k in d, k
+    assert d["n_gpus"] == 1 and d["steps"] == 20 and d["warmup"] == 3 and d["value"] > 0
+    assert d["dtype"] == "f64" and d["higher_is_better"] is True
+    r = d["roofline"]
+    for k in ("bound", "achieved", "peak", "unit", "frac", "traffic"):
+        assert k in r, k
+    assert r["peak"] > 0 and abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9
+    cb = d["cpu_baseline"]
+    for k in ("value", "unit", "cores", "kind", "sample"):
+        assert k in cb, k
+    assert cb["value"] > 0 and cb["sequential"]["cores"] == 1
+    e = d["e2e"]
+    assert 0 < e["value"] < d["value"] and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    assert d["clocks"]["sm_mhz"] and d["gpu_launches"] > 0
+    assert d["config"] == bench.workload_config("circular_dam_break", 10082, d["config"]["edges"],
+                                                d["config"]["boundary_edges"], 1)
