@@ -98,3 +98,31 @@ def test_b200_arm_line_carries_the_contract():
     assert d["clocks"]["sm_mhz"] and d["gpu_launches"] > 0
     assert d["config"] == bench.workload_config("circular_dam_break", 10082, d["config"]["edges"],
                                                 d["config"]["boundary_edges"], 1)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("scaling", ["strong", "weak"])
+def test_b200_arm_multi_rank_path_on_one_gpu(scaling):
+    """bench.py --gpus 2 under torch.distributed.run, both ranks on this one
+    GPU (SWE_BENCH_LOCKSTEP_CHECK=1: gloo, lockstep phases, no kernel waiting
+    on a concurrently running one): the N > 1 code path runs end to end and
+    its ranks agree on every step record."""
+    import os
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ, SWE_BENCH_LOCKSTEP_CHECK="1")
+    extra = ["--scale", "0.05"] if scaling == "strong" else ["--scaling", "weak", "--weak-base", "300"]
+    out = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                          "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                          str(port), str(ROOT / "bench.py"), "--gpus", "2", "--steps", "4",
+                          "--warmup", "3", *extra],
+                         cwd=ROOT, capture_output=True, text=True, timeout=900, env=env)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, out.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["lockstep_check"] is True and d["records_ok"] is True
+    assert d["n_gpus"] == 2 and d["steps"] == 4 and d["scaling"] == scaling
+    assert d["roofline"]["peak"] > 0 and d["e2e"]["value"] > 0
