@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--weak-base", type=int, default=2265,
                     help="weak scaling: generator nx at N=1 (default: SURVEY's 2265)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true",
+                    help="N > 1 strong scaling: keep the modelled split (no measured rebalancing)")
     ap.add_argument("--scaling", choices=["strong", "weak"], default="strong",
                     help="N > 1: strong = the configured mesh split N ways; weak = BASELINE "
                          "configs[4], the square water drop at ~10.26M cells per GPU")
@@ -311,6 +313,7 @@ def run_b200_dist(args, rank, local, world):
     import torch.distributed as tdist
     from paper_1807_00672_b200 import api, dist
 
+    dev = "cpu" if LOCKSTEP_CHECK else "cuda"  # the collectives' tensors (gloo / NCCL)
     if args.scaling == "weak":
         # BASELINE configs[4] / SURVEY §8(d) 5: the square water drop at ~10.26M
         # cells per GPU (nx = 2265, 3203, 4530, 6406 for N = 1, 2, 4, 8); every
@@ -329,9 +332,17 @@ def run_b200_dist(args, rank, local, world):
         sc, mesh, setup_s = build_workload(args.config, scale, device=local)
         C, E, NB = mesh.n_cells, mesh.n_edges, mesh.n_boundary_edges
         # equal work per GPU: cells weighted by the device's own dry-tile skip pattern
-        part = dist.partition(mesh, world, dist.measured_cost_weights(mesh, sc.state, device=local,
-                                                                      parts=world))
+        w0 = dist.measured_cost_weights(mesh, sc.state, device=local, parts=world)
+        part = dist.partition(mesh, world, w0)
+        if not args.no_rebalance:
+            t_r = time.perf_counter()
+            part, rebalance = rebalance_parts(args, mesh, sc.state, part, w0, rank, local, world,
+                                              dev, tdist, dist)
+            rebalance["s"] = round(time.perf_counter() - t_r, 2)
+            setup_s += rebalance["s"]
         lm = dist.local_mesh(mesh, part, rank)
+    if args.scaling == "weak" or args.no_rebalance:
+        rebalance = None
     lp = dist.LinkedPart(lm, device=local)
     inf = api.DeviceSolver.info(lp)
     U = inf["graph_unroll"]  # steps per WHILE iteration (graph loop)
@@ -345,7 +356,6 @@ def run_b200_dist(args, rank, local, world):
     lp.set_state(sc.state)
     horizon = HORIZON
     W, K = max(3, args.warmup), args.steps
-    dev = "cpu" if LOCKSTEP_CHECK else "cuda"
 
     def advance(target):  # run() segment up to step `target` (collective)
         if LOCKSTEP_CHECK:
@@ -436,7 +446,8 @@ def run_b200_dist(args, rank, local, world):
                           "trip per step)",
                    "cells_per_gpu_max": int(np.bincount(part).max()),
                    "cells_per_gpu_min": int(np.bincount(part).min()),
-                   "halo_cells_rank0": int(lm.n_cells - lm.n_owned)},
+                   "halo_cells_rank0": int(lm.n_cells - lm.n_owned),
+                   "rebalance": rebalance},
                "setup": {"setup_s": round(setup_s, 2)},
                "gpu_launches": 3 if PERSISTENT else 2 * U * -(-K // U) + 2,
                "gpu_launches_note": ("per rank: k_set_params, k_gate and one cooperative launch "
@@ -562,6 +573,36 @@ def weak_nx(world):
 
 def cfg_name(args):
     return "weak_square" if args.scaling == "weak" else args.config
+
+
+REBALANCE_ROUNDS = 2
+
+
+def rebalance_parts(args, mesh, state, part, w0, rank, local, world, dev, tdist, dist):
+    """Measured rebalancing of the strong-scaling split (dist.refine_weights):
+    every rank times its own part alone on its GPU (unlinked, its own dt), the
+    times are all-gathered, the cell weights scaled by each part's time and
+    the mesh re-split; after REBALANCE_ROUNDS the split whose slowest part was
+    fastest is kept (every rank takes the same decisions from the same
+    gathered times).  On one GPU (lockstep check) the ranks' timings contend,
+    so the choice there only exercises the code path."""
+    import torch
+    hist, best = [], None
+    w = w0
+    for r in range(REBALANCE_ROUNDS + 1):
+        mine = dist.part_step_ms(mesh, state, part, rank, device=local, steps=30)
+        t = torch.zeros(world, dtype=torch.float64, device=dev)
+        t[rank] = mine
+        tdist.all_reduce(t, op=tdist.ReduceOp.SUM)
+        times = [float(x) for x in t.cpu()]
+        hist.append(max(times))
+        if best is None or max(times) < best[0]:
+            best = (max(times), part, r)
+        if r == REBALANCE_ROUNDS:
+            break
+        w = dist.refine_weights(w, part, times)
+        part = dist.partition(mesh, world, w)
+    return best[1], {"rounds": REBALANCE_ROUNDS, "slowest_part_ms": hist, "kept_round": best[2]}
 
 
 def dist_roofline(C, E, K, ms, world, skip_frac, held_frac=0.0):
